@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py -- ICP point-pairs/s on B200 (BASELINE.json metric) for the north_star workload.
+
+Default workload (N=1): BASELINE.json configs[3], the ~2M-point LiDAR scan, point-to-plane,
+50 iterations, max dist 1.0 m -- the "2M-point config" the north_star target is quoted on.
+
+A STEP is one pass of the whole hot path over one synthetic
+frame pair already resident in HBM: cil_target_build (index over the target) followed by
+cil_icp_run (50 fused iterations: transform, exact 1-NN, reject, J^TJ/J^Tr, on-device solve
+and pose update).  value = source points x iterations / step time (pairs/s), whole job
+over all ranks.  L2 is flushed (a 512 MiB device write) before every timed step.
+
+--impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on the host cores
+on a bounded sample of the same workload; the driver computes the ratio itself.
+
+Multi-GPU (torchrun, one rank per GPU): every rank aligns its own independent frame pair
+(seed base 1807 + rank), no data-path collective: "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ICP point-pairs/sec per iteration (1-NN + 6x6 reduce); % of HBM roofline"
+UNIT = "point-pairs/s"
+
+
+def _workload(name: str, base: int):
+    import gen
+    if name == "c4_plane":
+        return gen.c4_lidar("point_to_plane", base=base)
+    if name == "c4_point":
+        return gen.c4_lidar("point_to_point", base=base)
+    if name == "c1":
+        return gen.c1_sphere(base=base)
+    if name == "c3":
+        w = gen.c3_depth(base=base)
+        raise SystemExit("c3 needs oracle PCA normals; bench it through tests/ instead")
+    if name.startswith("c5_"):
+        return gen.c5_patches(int(name[3:]), base=base)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def _bytes_per_pair(metric: str) -> int:
+    # 12 B source + 12 B target + 12 B normal (point-to-plane) per query
+    return 36 if metric == "point_to_plane" else 24
+
+
+def _peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1807_00399_b200 as cil
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = _workload(args.workload, 1807 + rank)
+    iters = args.iters or w.max_iters
+    metric = w.metric
+    to_dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
+    tgt = to_dev(w.target)
+    nrm = to_dev(w.target_normals) if w.target_normals is not None else None
+    src = to_dev(w.source)
+    P0 = to_dev(np.eye(4))
+    prm = cil.make_params(metric, iters, w.max_dist)
+    ws = cil.alloc_workspace(w.m, prm, dev)
+    res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        t = cil.cil_target_build(tgt, nrm, args.leaf)
+        if evs:
+            evs[1].record(stream)
+        cil.cil_icp_run(t, src, P0, prm, ws=ws, res=res, want_log=False)
+        t.free()
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, L2 flushed before each; events on the launching stream
+    launches0 = cil.launch_count()
+    tot_ms, build_ms, run_ms = 0.0, 0.0, 0.0
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            evs[0].record(stream)
+            step(evs)
+            evs[2].record(stream)
+            evs[2].synchronize()
+            tot_ms += evs[0].elapsed_time(evs[2])
+            build_ms += evs[0].elapsed_time(evs[1])
+            run_ms += evs[1].elapsed_time(evs[2])
+        torch.cuda.synchronize()
+    launches = cil.launch_count() - launches0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_max = float(t.item())
+        pairs = torch.tensor([float(w.m) * iters * args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(pairs, op=dist.ReduceOp.SUM)
+        total_pairs = float(pairs.item())
+        dist.barrier()
+    else:
+        tot_max, total_pairs = tot_ms, float(w.m) * iters * args.steps
+    r = cil.decode_result(res)
+    if rank != 0:
+        return None
+    ms_step = tot_max / args.steps
+    value = total_pairs / (tot_max / 1e3)
+    # dominant kernel: the fused iteration; its average launch = run time / iterations
+    # (run = init + iters x icp_iter_kernel + final, so this slightly overstates the launch)
+    it_ms = (run_ms / args.steps) / iters
+    bpp = _bytes_per_pair(metric)
+    achieved = bpp * w.m / (it_ms * 1e-3) / 1e9
+    peak, peak_src = _peak_hbm()
+    traffic = _traffic_from_profiles(args.workload)
+
+    # e2e: the public host-buffer API (pinned host inputs, H2D inside the timed region,
+    # result read back to the host every step)
+    e2e = _e2e(args, w, iters, cil, dev, flush) if not args.no_e2e else None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {
+            "workload": f"{w.name}: BASELINE.json configs[3] LiDAR 64x31250, {metric}, {iters} iterations, "
+                        f"max dist {w.max_dist} m (target build + ICP run per step)",
+            "n_target": w.n, "n_source": w.m, "iterations": iters, "leaf_size": args.leaf or 8,
+            "l2": "flushed before every step (512 MiB device write)",
+            "build_ms": build_ms / args.steps, "icp_ms_per_iteration": it_ms,
+            "final_status": r.status, "final_n_corr": r.n_corr, "final_rmse": r.rmse,
+            "parallelism": f"independent frame pair per rank x{world}",
+        },
+        "roofline": {"bound": "hbm", "kernel": "icp_iter_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "bytes_per_pair": bpp, "peak_source": peak_src,
+                     "frac_of_8TBps_nominal": achieved / 8000.0},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = _cpu_baseline(w, metric, args)
+    return out
+
+
+def C_sizeof(ct):
+    import ctypes
+    return ctypes.sizeof(ct)
+
+
+def _traffic_from_profiles(workload):
+    """dram bytes per icp_iter_kernel launch from the committed ncu --set full summary"""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+def _e2e(args, w, iters, cil, dev, flush):
+    import torch
+    stream = torch.cuda.current_stream()
+    h_t = torch.as_tensor(w.target).pin_memory()
+    h_n = torch.as_tensor(w.target_normals).pin_memory() if w.target_normals is not None else None
+    h_s = torch.as_tensor(w.source).pin_memory()
+    h_res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8).pin_memory()
+    d_t = torch.empty_like(h_t, device=dev)
+    d_n = torch.empty_like(h_n, device=dev) if h_n is not None else None
+    d_s = torch.empty_like(h_s, device=dev)
+    P0 = torch.eye(4, dtype=torch.float64, device=dev)
+    prm = cil.make_params(w.metric, iters, w.max_dist)
+    ws = cil.alloc_workspace(w.m, prm, dev)
+    res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8, device=dev)
+
+    def step():
+        d_t.copy_(h_t, non_blocking=True)
+        if d_n is not None:
+            d_n.copy_(h_n, non_blocking=True)
+        d_s.copy_(h_s, non_blocking=True)
+        t = cil.cil_target_build(d_t, d_n, args.leaf)
+        cil.cil_icp_run(t, d_s, P0, prm, ws=ws, res=res, want_log=False)
+        h_res.copy_(res, non_blocking=True)
+        t.free()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    h2d = h_t.numel() * 4 + (h_n.numel() * 4 if h_n is not None else 0) + h_s.numel() * 4
+    return {"value": w.m * iters * args.steps / (tot / 1e3), "unit": UNIT, "ms_per_step": tot / args.steps,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h_res.numel())}
+
+
+# ---------------------------------------------------------------------------- oracle arm
+def _oracle_sample(w, metric, sample_pts, iters, threads):
+    """the oracle as it stands: kd-tree over the full target, ICP on a seeded subset of the
+    source (same pose sequence semantics: identity init, fixed iterations)"""
+    import oracle
+    if threads:
+        oracle.set_threads(threads)
+    rng = np.random.default_rng(7)
+    sel = np.sort(rng.choice(w.m, size=min(sample_pts, w.m), replace=False))
+    src = np.ascontiguousarray(w.source[sel])
+    t0 = time.perf_counter()
+    tree = oracle.KDTree(w.target)
+    t1 = time.perf_counter()
+    res = oracle.icp_run(None, w.target_normals, src, metric, iters, w.max_dist, tree=tree)
+    t2 = time.perf_counter()
+    return {"value": len(sel) * iters / (t2 - t0), "build_s": t1 - t0, "icp_s": t2 - t1, "pairs": len(sel) * iters,
+            "cores": oracle.get_threads(), "status": res.status}
+
+
+def _cpu_baseline(w, metric, args):
+    iters = args.iters or w.max_iters
+    r = _oracle_sample(w, metric, args.cpu_sample, iters, 0)
+    return {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+            "sample": f"{r['pairs'] // iters} of {w.m} source points (seeded subset) x {iters} iterations against "
+                      f"the full {w.n}-point target, incl. kd-tree build ({r['build_s']:.2f} s + icp {r['icp_s']:.2f} s)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    w = _workload(args.workload, 1807)
+    iters = args.iters or w.max_iters
+    import oracle
+    for _ in range(args.warmup):
+        _oracle_sample(w, w.metric, max(1024, args.cpu_sample // 16), 1, 0)
+    tot = 0.0
+    pairs = 0
+    for _ in range(args.steps):
+        r = _oracle_sample(w, w.metric, args.cpu_sample, iters, 0)
+        tot += r["build_s"] + r["icp_s"]
+        pairs += r["pairs"]
+    value = pairs / tot
+    sample = (f"{args.cpu_sample} of {w.m} source points (seeded subset) x {iters} iterations against the full "
+              f"{w.n}-point target per step, incl. kd-tree build")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: BASELINE.json configs[3], {w.metric}, {iters} iterations, "
+                                   f"max dist {w.max_dist} m", "n_target": w.n, "n_source": w.m},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4_plane")
+    ap.add_argument("--iters", type=int, default=0, help="override the config's iteration count")
+    ap.add_argument("--leaf", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+        out = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * cil.h -- C ABI of the B200-native ICP hot path (libcil.so).
+ *
+ * The operation is one rigid ICP iteration as the cilantro paper (arXiv 1807.00399)
+ * states it: "the top-level loop logic (alternating between correspondence estimation
+ * and transformation parameter optimization) of the Iterative Closest Point (ICP)
+ * algorithm ... parameterized by the correspondence estimation mechanism and the transform
+ * estimator ... a standard, kd-tree based correspondence search engine ... optimizers for
+ * rigid [Besl & McKay; Low] ... registration under the point-to-point and point-to-plane
+ * metrics" (section "Functionality / Iterative geometric registration"),
+ * run with "nearest neighbor kd-tree queries, with a rejection distance threshold" and
+ * "a fixed number of ... iterations" (section "Performance").
+ * Inputs are matrix views with "one data point per column ... contiguously stored in
+ * memory, in column-major order": for D = 3 this is packed fp32 x,y,z,x,y,z...
+ *
+ * Conventions (every function):
+ *   - Every array pointer is a DEVICE pointer unless stated otherwise.  Calls are
+ *     stream-ordered and asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and never synchronise the device.
+ *   - Points and normals: packed fp32 xyz, element i at [3*i .. 3*i+2], 4-byte aligned.
+ *   - Poses: 4x4 row-major fp64 matrices mapping SOURCE coordinates to TARGET coordinates,
+ *     [R t; 0 0 0 1] (reading R5: increments are left-composed).
+ *   - Counts n, m: 0 <= m, 1 <= n, both <= INT32_MAX.
+ *   - Ownership: the caller owns every input, output and workspace buffer; the library
+ *     keeps no caller pointer beyond the enqueued work.  A cil_target owns its device
+ *     buffers (allocated stream-ordered on the build stream, freed by cil_target_free).
+ *     A built target is immutable: concurrent queries on different streams are allowed,
+ *     each with its own workspace; a workspace must not be shared by concurrent calls.
+ *   - Errors: host-detectable problems (NULL pointers, bad sizes or parameters, missing
+ *     normals for point-to-plane, small or misaligned workspace, CUDA launch failures)
+ *     are returned synchronously, before anything is enqueued when possible.  Data-
+ *     dependent outcomes (degenerate 6x6 system, zero correspondences) are written on the
+ *     device into the .status field of the result/system structs.  The library never
+ *     aborts and never prints.  cil_last_error() gives a thread-local detail string.
+ *   - No CPU fallback exists: every step runs in the library's own sm_100a kernels.
+ */
+#ifndef CIL_H_
+#define CIL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A cudaStream_t (identical type: pointer to the opaque CUDA stream struct). */
+typedef struct CUstream_st* cil_stream_t;
+
+typedef enum {
+    CIL_OK = 0,
+    CIL_ERR_INVALID_ARG = 1,   /* NULL pointer, n/m out of range, bad metric, max_dist <= 0 ... */
+    CIL_ERR_EMPTY_TARGET = 2,  /* n == 0 ("errors: empty target") */
+    CIL_ERR_NO_NORMALS = 3,    /* point-to-plane on a target built without normals */
+    CIL_ERR_CUDA = 4,          /* a CUDA runtime call or launch failed; see cil_last_error() */
+    CIL_ERR_OOM = 5,           /* device allocation failed */
+    CIL_ERR_WORKSPACE = 6,     /* ws NULL, misaligned (needs 256 B) or smaller than required */
+    /* reported on the device in cil_icp_result.status / cil_icp_system.status: */
+    CIL_ERR_DEGENERATE = 16,       /* count < 6, Cholesky pivot <= 0 or min/max pivot < 1e-12 (R9) */
+    CIL_NO_CORRESPONDENCES = 17    /* no pair within max_corr_dist (R10) */
+} cil_status;
+
+typedef enum {
+    CIL_POINT_TO_POINT = 0,    /* r = s - t,        J = [-[s]x , I3]  [Besl & McKay]  */
+    CIL_POINT_TO_PLANE = 1     /* r = (s - t).n,    J = [s x n ; n]   [Low 2004]      */
+} cil_metric;
+
+typedef struct cil_target cil_target;   /* opaque, immutable after build */
+
+/* Spatial-index parameters (NULL = defaults).  leaf_size: points per BVH leaf
+   (0 = default 8; 1..32).  Other fields reserved, must be 0. */
+typedef struct {
+    int32_t leaf_size;
+    int32_t reserved[7];
+} cil_index_params;
+
+/* ICP parameters.  metric: cil_metric.  max_iters >= 1 (cil_icp_run only).
+   max_corr_dist > 0: pairs with |s - t| > max_corr_dist are rejected (inclusive bound,
+   PAPER.md:195, R2).  rot_tol (rad) / trans_tol: cil_icp_run stops after an
+   iteration whose increment has angle < rot_tol AND |tau| < trans_tol (both 0 = fixed
+   iteration count).  w_point/w_plane: reserved for the combined metric
+   (must be 0). */
+typedef struct {
+    int32_t metric;
+    int32_t max_iters;
+    double max_corr_dist;
+    double rot_tol;
+    double trans_tol;
+    double w_point;
+    double w_plane;
+} cil_icp_params;
+
+/* Result of cil_icp_run, written on the device.  rmse = sqrt(sum r^2 / n_corr) over the
+   accepted pairs of the last executed iteration, before its update (R11); iterations =
+   number of executed iterations (an iteration that finds no pair or a degenerate system
+   counts, and stops the loop with the pose unchanged). */
+typedef struct {
+    double pose[16];
+    double rmse;
+    int64_t n_corr;
+    int32_t iterations;
+    int32_t converged;
+    int32_t status;     /* CIL_OK, CIL_ERR_DEGENERATE or CIL_NO_CORRESPONDENCES */
+    int32_t pad;
+} cil_icp_result;
+
+/* The normal equations of one iteration, written on the device: H (6x6 row-major,
+   symmetric), g (6), sse = sum of squared residuals, n_corr accepted pairs; x = the
+   increment -H^-1 g (alpha = x[0:3], tau = x[3:6]; zeros when status != CIL_OK). */
+typedef struct {
+    double H[36];
+    double g[6];
+    double x[6];
+    double sse;
+    int64_t n_corr;
+    int32_t status;
+    int32_t pad;
+} cil_icp_system;
+
+/* Host-readable description of a built target. */
+typedef struct {
+    int64_t n;            /* number of target points */
+    int64_t n_leaves;     /* BVH leaves */
+    int64_t n_nodes;      /* implicit binary-tree node slots (2 * next_pow2(n_leaves)) */
+    int32_t leaf_size;
+    int32_t has_normals;
+    int64_t device_bytes; /* bytes owned by the target */
+} cil_target_info;
+
+/* Build the spatial index over the target (BASELINE.json north_star
+   "(2) a GPU spatial index over the target ... Morton-sorted cells built by a device radix
+   sort"): bounding box -> 63-bit Morton keys -> radix sort -> reorder points/normals ->
+   leaf and node AABBs of an implicit binary BVH.
+   pts [n*3] fp32 device; normals [n*3] fp32 device or NULL (required for point-to-plane).
+   On success *out receives the new target (host handle).  The inputs may be freed after
+   the stream reaches the end of the enqueued work. */
+cil_status cil_target_build(const float* pts, const float* normals, int64_t n,
+                            const cil_index_params* params, cil_stream_t stream, cil_target** out);
+
+/* Release a target (stream-ordered free on `stream`). NULL is a no-op. */
+cil_status cil_target_free(cil_target* t, cil_stream_t stream);
+
+/* Host-only: describe a target. */
+cil_status cil_target_get_info(const cil_target* t, cil_target_info* info);
+
+/* Exact 1-NN ("k-NN ... queries"): for each query q_i
+   (packed fp32 xyz [m*3]) find argmin_j |q_i - t_j|^2 over the target, ties to the lowest
+   ORIGINAL target index (R1).  max_dist: only targets with |q - t| <= max_dist count
+   (INFINITY = unbounded).  Outputs in query order: idx[m] int32 original target index or -1,
+   sqdist[m] fp32 squared distance or +INF (BASELINE.json configs[1] "output nearest index
+   (int32) and squared distance").  Either output may be NULL. m == 0 is a no-op. */
+cil_status cil_nn_query(const cil_target* t, const float* queries, int64_t m, float max_dist,
+                        int32_t* idx, float* sqdist, cil_stream_t stream);
+
+/* Host-only: exact workspace size in bytes for cil_icp_iterate / cil_icp_run on m
+   source points (the same size serves both).  Returns 0 for invalid arguments. */
+size_t cil_icp_workspace_bytes(int64_t m, const cil_icp_params* params);
+
+/* One stateless ICP iteration: s_i = R p_i + t (fp64 pose,
+   double-float s), exact 1-NN of s_i, reject |s_i - t_j| > max_corr_dist, accumulate
+   H = sum J^T J and g = sum J^T r for the chosen metric, solve H x = -g (6x6 Cholesky,
+   fp64) and write pose_out = [exp([alpha]x) R, exp([alpha]x) t + tau].
+   src [m*3] fp32; pose_in/pose_out fp64[16] device (may alias: in-place update);
+   ws: device workspace (256-B aligned, >= cil_icp_workspace_bytes(m, params)).
+   Optional outputs (NULL to skip): sys (device cil_icp_system), corr_idx[m] (int32
+   original target index or -1 when rejected), corr_sqdist[m] (fp32 d^2 or +INF).
+   On a degenerate system or zero correspondences pose_out = pose_in and sys->status
+   says why. */
+cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_t m, const double* pose_in,
+                           const cil_icp_params* params, void* ws, size_t ws_bytes, double* pose_out,
+                           cil_icp_system* sys, int32_t* corr_idx, float* corr_sqdist,
+                           cil_stream_t stream);
+
+/* The ICP loop for params->max_iters iterations with no host round-trip:
+   every iteration is enqueued up front; the pose and the stop flag live in device memory,
+   so iterations after convergence, degeneracy or zero correspondences do no work.
+   pose_init fp64[16] device; res: device cil_icp_result; iter_log (nullable) device
+   fp64[max_iters*2] = {n_corr, rmse} per executed iteration (unexecuted rows are 0). */
+cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                       const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                       double* iter_log, cil_stream_t stream);
+
+/* Static strings; cil_last_error is thread-local detail for the last failing call. */
+const char* cil_status_string(cil_status s);
+const char* cil_last_error(void);
+
+/* Build/version info (static string). */
+const char* cil_version(void);
+
+/* Diagnostics: number of kernels this process has enqueued through the library so far
+   (host counter, incremented at every launch). */
+uint64_t cil_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIL_H_ */

@@ -1,0 +1,316 @@
+"""paper_1807_00399_b200 -- thin Python binding over libcil.so (include/cil.h).
+
+The binding only marshals arguments: torch tensors provide device memory and the CUDA
+stream (torch.cuda.current_stream() by default); every step of the ICP hot path runs in
+the library's own sm_100a kernels.  There is no CPU fallback: importing this package
+fails loudly if libcil.so is missing, and every call raises CilError on failure.
+
+Function names match the C ABI (cil_target_build, cil_nn_query, cil_icp_workspace_bytes,
+cil_icp_iterate, cil_icp_run, cil_target_free).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcil.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libcil.so not built at {LIB_PATH}: run `make` or __graft_entry__.build(); "
+                      "there is no CPU fallback for the ICP hot path")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- status / structs
+CIL_OK = 0
+CIL_ERR_INVALID_ARG = 1
+CIL_ERR_EMPTY_TARGET = 2
+CIL_ERR_NO_NORMALS = 3
+CIL_ERR_CUDA = 4
+CIL_ERR_OOM = 5
+CIL_ERR_WORKSPACE = 6
+CIL_ERR_DEGENERATE = 16
+CIL_NO_CORRESPONDENCES = 17
+CIL_POINT_TO_POINT = 0
+CIL_POINT_TO_PLANE = 1
+METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_PLANE}
+
+EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
+            "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
+            "cil_last_error", "cil_version", "cil_launch_count"]
+
+
+class cil_index_params(C.Structure):
+    _fields_ = [("leaf_size", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+class cil_icp_params(C.Structure):
+    _fields_ = [("metric", C.c_int32), ("max_iters", C.c_int32), ("max_corr_dist", C.c_double),
+                ("rot_tol", C.c_double), ("trans_tol", C.c_double), ("w_point", C.c_double),
+                ("w_plane", C.c_double)]
+
+
+class cil_icp_result(C.Structure):
+    _fields_ = [("pose", C.c_double * 16), ("rmse", C.c_double), ("n_corr", C.c_int64),
+                ("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+class cil_icp_system(C.Structure):
+    _fields_ = [("H", C.c_double * 36), ("g", C.c_double * 6), ("x", C.c_double * 6), ("sse", C.c_double),
+                ("n_corr", C.c_int64), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+class cil_target_info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_leaves", C.c_int64), ("n_nodes", C.c_int64), ("leaf_size", C.c_int32),
+                ("has_normals", C.c_int32), ("device_bytes", C.c_int64)]
+
+
+_vp, _i64, _sz = C.c_void_p, C.c_int64, C.c_size_t
+_lib.cil_target_build.restype = C.c_int
+_lib.cil_target_build.argtypes = [_vp, _vp, _i64, C.POINTER(cil_index_params), _vp, C.POINTER(_vp)]
+_lib.cil_target_free.restype = C.c_int
+_lib.cil_target_free.argtypes = [_vp, _vp]
+_lib.cil_target_get_info.restype = C.c_int
+_lib.cil_target_get_info.argtypes = [_vp, C.POINTER(cil_target_info)]
+_lib.cil_nn_query.restype = C.c_int
+_lib.cil_nn_query.argtypes = [_vp, _vp, _i64, C.c_float, _vp, _vp, _vp]
+_lib.cil_icp_workspace_bytes.restype = _sz
+_lib.cil_icp_workspace_bytes.argtypes = [_i64, C.POINTER(cil_icp_params)]
+_lib.cil_icp_iterate.restype = C.c_int
+_lib.cil_icp_iterate.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp, _vp, _vp]
+_lib.cil_icp_run.restype = C.c_int
+_lib.cil_icp_run.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp]
+_lib.cil_status_string.restype = C.c_char_p
+_lib.cil_status_string.argtypes = [C.c_int]
+_lib.cil_last_error.restype = C.c_char_p
+_lib.cil_version.restype = C.c_char_p
+_lib.cil_launch_count.restype = C.c_uint64
+
+
+def launch_count() -> int:
+    """kernels enqueued by libcil.so in this process so far"""
+    return int(_lib.cil_launch_count())
+
+
+class CilError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = f"{where}: {_lib.cil_status_string(status).decode()} ({_lib.cil_last_error().decode()})"
+        super().__init__(msg)
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != CIL_OK:
+        raise CilError(rc, where)
+
+
+def version() -> str:
+    return _lib.cil_version().decode()
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _pts(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.dim() == 2
+            and t.shape[1] == 3 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous CUDA float32 tensor of shape [n, 3]")
+    return t
+
+
+def make_params(metric: str | int = "point_to_plane", max_iters: int = 1, max_corr_dist: float = math.inf,
+                rot_tol: float = 0.0, trans_tol: float = 0.0) -> cil_icp_params:
+    p = cil_icp_params()
+    p.metric = METRICS[metric] if isinstance(metric, str) else int(metric)
+    p.max_iters = int(max_iters)
+    p.max_corr_dist = float(max_corr_dist)
+    p.rot_tol = float(rot_tol)
+    p.trans_tol = float(trans_tol)
+    p.w_point = 0.0
+    p.w_plane = 0.0
+    return p
+
+
+# ---------------------------------------------------------------- ABI-named entry points
+class Target:
+    """Owning handle of a cil_target (built on the GPU, immutable)."""
+
+    def __init__(self, handle: int, n: int, keep=()):
+        self.handle = handle
+        self.n = n
+        self._keep = keep
+
+    def info(self) -> cil_target_info:
+        inf = cil_target_info()
+        _check(_lib.cil_target_get_info(self.handle, C.byref(inf)), "cil_target_get_info")
+        return inf
+
+    def free(self, stream=None) -> None:
+        if self.handle:
+            _check(_lib.cil_target_free(self.handle, _stream_ptr(stream)), "cil_target_free")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            if self.handle and torch.cuda.is_available():
+                _lib.cil_target_free(self.handle, None)
+        except Exception:
+            pass
+
+
+def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, leaf_size: int = 0,
+                     stream=None) -> Target:
+    _pts(pts, "pts")
+    if normals is not None:
+        _pts(normals, "normals")
+        if normals.shape != pts.shape:
+            raise ValueError("normals must match pts")
+    prm = cil_index_params()
+    prm.leaf_size = int(leaf_size)
+    h = _vp()
+    _check(_lib.cil_target_build(_ptr(pts), _ptr(normals), pts.shape[0], C.byref(prm), _stream_ptr(stream),
+                                 C.byref(h)), "cil_target_build")
+    return Target(h.value, pts.shape[0])
+
+
+def cil_target_free(t: Target, stream=None) -> None:
+    t.free(stream)
+
+
+def cil_nn_query(t: Target, queries: torch.Tensor, max_dist: float = math.inf, stream=None,
+                 idx: torch.Tensor | None = None, sqdist: torch.Tensor | None = None):
+    _pts(queries, "queries")
+    m = queries.shape[0]
+    dev = queries.device
+    if idx is None:
+        idx = torch.empty(m, dtype=torch.int32, device=dev)
+    if sqdist is None:
+        sqdist = torch.empty(m, dtype=torch.float32, device=dev)
+    _check(_lib.cil_nn_query(t.handle, _ptr(queries), m, float(max_dist), _ptr(idx), _ptr(sqdist),
+                             _stream_ptr(stream)), "cil_nn_query")
+    return idx, sqdist
+
+
+def cil_icp_workspace_bytes(m: int, params: cil_icp_params) -> int:
+    return int(_lib.cil_icp_workspace_bytes(int(m), C.byref(params)))
+
+
+def alloc_workspace(m: int, params: cil_icp_params, device="cuda") -> torch.Tensor:
+    nb = cil_icp_workspace_bytes(m, params)
+    if nb == 0:
+        raise ValueError("invalid workspace request")
+    return torch.empty(nb, dtype=torch.uint8, device=device)   # caching allocator: >= 512-B aligned
+
+
+def _struct_tensor(ctype, device) -> torch.Tensor:
+    return torch.zeros(C.sizeof(ctype), dtype=torch.uint8, device=device)
+
+
+def read_struct(t: torch.Tensor, ctype):
+    return ctype.from_buffer_copy(t.cpu().numpy().tobytes())
+
+
+def cil_icp_iterate(t: Target, src: torch.Tensor, pose_in: torch.Tensor, params: cil_icp_params,
+                    ws: torch.Tensor | None = None, pose_out: torch.Tensor | None = None,
+                    want_sys: bool = True, want_corr: bool = False, stream=None):
+    """One stateless ICP iteration.  Returns (pose_out [4,4] f64 device, sys_bytes device
+    tensor or None, corr_idx or None, corr_sqdist or None)."""
+    _pts(src, "src")
+    m = src.shape[0]
+    dev = src.device
+    if ws is None:
+        ws = alloc_workspace(m, params, dev)
+    if pose_out is None:
+        pose_out = torch.empty((4, 4), dtype=torch.float64, device=dev)
+    sys_t = _struct_tensor(cil_icp_system, dev) if want_sys else None
+    ci = torch.empty(m, dtype=torch.int32, device=dev) if want_corr else None
+    cd = torch.empty(m, dtype=torch.float32, device=dev) if want_corr else None
+    _check(_lib.cil_icp_iterate(t.handle, _ptr(src), m, _ptr(pose_in), C.byref(params), _ptr(ws), ws.numel(),
+                                _ptr(pose_out), _ptr(sys_t), _ptr(ci), _ptr(cd), _stream_ptr(stream)),
+           "cil_icp_iterate")
+    return pose_out, sys_t, ci, cd
+
+
+def cil_icp_run(t: Target, src: torch.Tensor, pose_init: torch.Tensor, params: cil_icp_params,
+                ws: torch.Tensor | None = None, res: torch.Tensor | None = None, iter_log: torch.Tensor | None = None,
+                want_log: bool = True, stream=None):
+    """The device-resident ICP loop.  Returns (res_bytes device tensor, iter_log [max_iters,2] or None)."""
+    _pts(src, "src")
+    m = src.shape[0]
+    dev = src.device
+    if ws is None:
+        ws = alloc_workspace(m, params, dev)
+    if res is None:
+        res = _struct_tensor(cil_icp_result, dev)
+    if iter_log is None and want_log:
+        iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev)
+    _check(_lib.cil_icp_run(t.handle, _ptr(src), m, _ptr(pose_init), C.byref(params), _ptr(ws), ws.numel(),
+                            _ptr(res), _ptr(iter_log), _stream_ptr(stream)), "cil_icp_run")
+    return res, iter_log
+
+
+# ---------------------------------------------------------------- decoded views
+@dataclass
+class System:
+    H: np.ndarray
+    g: np.ndarray
+    x: np.ndarray
+    sse: float
+    n_corr: int
+    status: int
+
+
+@dataclass
+class Result:
+    pose: np.ndarray
+    rmse: float
+    n_corr: int
+    iterations: int
+    converged: bool
+    status: int
+
+
+def decode_system(t: torch.Tensor) -> System:
+    s = read_struct(t, cil_icp_system)
+    return System(np.array(s.H).reshape(6, 6), np.array(s.g), np.array(s.x), s.sse, s.n_corr, s.status)
+
+
+def decode_result(t: torch.Tensor) -> Result:
+    r = read_struct(t, cil_icp_result)
+    return Result(np.array(r.pose).reshape(4, 4), r.rmse, r.n_corr, r.iterations, bool(r.converged), r.status)
+
+
+def icp_align(target_pts, target_normals, source_pts, metric="point_to_plane", max_iters=30, max_corr_dist=0.05,
+              pose_init=None, rot_tol=0.0, trans_tol=0.0, leaf_size=0, device="cuda", stream=None) -> Result:
+    """End-to-end public call from HOST arrays (numpy or CPU tensors): host->device copies,
+    target build, the device-resident ICP loop, and a device->host read of the result."""
+    def to_dev(a):
+        if a is None:
+            return None
+        ta = torch.as_tensor(a)
+        return ta.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
+    tp, tn, sp = to_dev(target_pts), to_dev(target_normals), to_dev(source_pts)
+    P0 = torch.as_tensor(np.eye(4) if pose_init is None else np.asarray(pose_init, np.float64)).to(device)
+    prm = make_params(metric, max_iters, max_corr_dist, rot_tol, trans_tol)
+    tgt = cil_target_build(tp, tn, leaf_size, stream)
+    res, _ = cil_icp_run(tgt, sp, P0, prm, want_log=False, stream=stream)
+    out = decode_result(res)
+    tgt.free(stream)
+    return out

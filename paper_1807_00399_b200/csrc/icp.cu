@@ -1,0 +1,488 @@
+// icp.cu -- the fused ICP iteration and the device-resident
+// loop.  BASELINE.json north_star subsystems (4) "the fused transform+reject+J^TJ/J^Tr kernel,
+// with per-warp shuffle reductions and per-block fp32 partials reduced in fp64" and (5) "the
+// on-device 6x6 Cholesky solve and pose update, so an iteration loop launches with no host
+// round-trip".
+//
+// One launch = one iteration:
+//   every thread, for its queries i = tid, tid + stride, ...:
+//     a1  s = R p_i + t (fp64) -> double-float
+//     a2  exact 1-NN over the BVH, bounded by max_corr_dist (warm-started in cil_icp_run by
+//         the previous iteration's match, which only tightens the initial bound)
+//     a3  reject: accepted iff a target with d^2 <= fl32(max_corr_dist^2) exists
+//     a4  residual + Jacobian of the metric (PAPER.md:140 [Besl], [Low])
+//     a5  fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
+//   warp: transposed butterfly reduce (31 SHFL for 32 values; lane k ends with sum k)
+//   block: per-warp fp64 sums -> per-CTA fp64 partial in the workspace
+//   last CTA (ticket): ordered fp64 sum of the partials -> a6 Cholesky solve -> a7 pose update,
+//   status, log.  Results are bitwise reproducible run to run (fixed grid, fixed orders,
+//   no floating-point atomics).
+#include "internal.cuh"
+#include "search.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace cil {
+namespace {
+
+constexpr int kIcpThreads = 256;
+constexpr int kIcpWarps = kIcpThreads / 32;
+
+struct IterArgs {
+    TargetView T;
+    const float* src;
+    int m;
+    float bound2;
+    const double* pose_in;
+    double* pose_out;
+    double* partials;        // [kMaxCtas * kSlots]
+    IcpState* st;
+    cil_icp_system* sys;     // iterate only, nullable
+    int32_t* corr_idx;       // iterate only, nullable
+    float* corr_d2;          // iterate only, nullable
+    int* nn_prev;            // run only: warm-start match per query (sorted target position or -1)
+    double* iter_log;        // run only, nullable
+    int run;
+    double rot_tol, trans_tol;
+};
+
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[kSlots]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+            float send = upper ? v[j] : v[j + off];
+            float keep = upper ? v[j + off] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+// ---------------------------------------------------------------- a6 + a7 (one thread)
+__device__ void rodrigues(const double a[3], double R[9]) {
+    const double th2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+    const double th = sqrt(th2);
+    double A, Bc;
+    if (th < 1e-4) { A = 1.0 - th2 / 6.0; Bc = 0.5 - th2 / 24.0; }
+    else { double sn, cs; sincos(th, &sn, &cs); A = sn / th; Bc = (1.0 - cs) / th2; }
+    // R = I + A [a]x + Bc [a]x^2,  [a]x^2 = a a^T - th2 I
+    R[0] = 1.0 + Bc * (a[0] * a[0] - th2);
+    R[4] = 1.0 + Bc * (a[1] * a[1] - th2);
+    R[8] = 1.0 + Bc * (a[2] * a[2] - th2);
+    R[1] = -A * a[2] + Bc * a[0] * a[1];
+    R[3] = A * a[2] + Bc * a[0] * a[1];
+    R[2] = A * a[1] + Bc * a[0] * a[2];
+    R[6] = -A * a[1] + Bc * a[0] * a[2];
+    R[5] = -A * a[0] + Bc * a[1] * a[2];
+    R[7] = A * a[0] + Bc * a[1] * a[2];
+}
+
+// Build (H, g, sse, count) from the reduced sums of the metric.
+template <int METRIC>
+__device__ void assemble(const double* S, double H[36], double g[6], double& sse, double& cnt) {
+    if (METRIC == CIL_POINT_TO_PLANE) {
+        int k = 0;
+        for (int a = 0; a < 6; ++a)
+            for (int b = a; b < 6; ++b, ++k) { H[6 * a + b] = S[k]; H[6 * b + a] = S[k]; }
+        for (int a = 0; a < 6; ++a) g[a] = S[21 + a];
+        sse = S[27];
+        cnt = S[28];
+    } else {
+        cnt = S[0];
+        const double Sx = S[1], Sy = S[2], Sz = S[3];
+        const double xx = S[4], yy = S[5], zz = S[6], xy = S[7], xz = S[8], yz = S[9];
+        // H_rr = sum(|s|^2 I - s s^T), formed from the diagonal sums (no cancellation)
+        H[0] = yy + zz; H[1] = -xy;     H[2] = -xz;
+        H[6] = -xy;     H[7] = xx + zz; H[8] = -yz;
+        H[12] = -xz;    H[13] = -yz;    H[14] = xx + yy;
+        // H_rt = [sum s]x, H_tr = H_rt^T, H_tt = count I
+        const double Hrt[9] = {0.0, -Sz, Sy, Sz, 0.0, -Sx, -Sy, Sx, 0.0};
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                H[6 * a + 3 + b] = Hrt[3 * a + b];
+                H[6 * (3 + b) + a] = Hrt[3 * a + b];
+                H[6 * (3 + a) + 3 + b] = a == b ? cnt : 0.0;
+            }
+        g[0] = S[13]; g[1] = S[14]; g[2] = S[15];   // sum s x r
+        g[3] = S[10]; g[4] = S[11]; g[5] = S[12];   // sum r
+        sse = S[16];
+    }
+}
+
+// Cholesky solve of H x = -g with the degeneracy rule of DESIGN.md R9; returns status.
+__device__ int solve6(const double H[36], const double g[6], double cnt, double x[6]) {
+    for (int i = 0; i < 6; ++i) x[i] = 0.0;
+    if (cnt == 0.0) return CIL_NO_CORRESPONDENCES;
+    if (cnt < 6.0) return CIL_ERR_DEGENERATE;
+    double L[36];
+    double pmin = INFINITY, pmax = 0.0;
+    for (int j = 0; j < 6; ++j) {
+        double d = H[6 * j + j];
+        for (int k = 0; k < j; ++k) d -= L[6 * j + k] * L[6 * j + k];
+        if (!(d > 0.0)) return CIL_ERR_DEGENERATE;
+        pmin = fmin(pmin, d);
+        pmax = fmax(pmax, d);
+        const double ljj = sqrt(d);
+        L[6 * j + j] = ljj;
+        const double inv = 1.0 / ljj;
+        for (int i = j + 1; i < 6; ++i) {
+            double v = H[6 * i + j];
+            for (int k = 0; k < j; ++k) v -= L[6 * i + k] * L[6 * j + k];
+            L[6 * i + j] = v * inv;
+        }
+    }
+    if (pmin < 1e-12 * pmax) return CIL_ERR_DEGENERATE;
+    double y[6];
+    for (int i = 0; i < 6; ++i) {
+        double v = -g[i];
+        for (int k = 0; k < i; ++k) v -= L[6 * i + k] * y[k];
+        y[i] = v / L[6 * i + i];
+    }
+    for (int i = 5; i >= 0; --i) {
+        double v = y[i];
+        for (int k = i + 1; k < 6; ++k) v -= L[6 * k + i] * x[k];
+        x[i] = v / L[6 * i + i];
+    }
+    return CIL_OK;
+}
+
+template <int METRIC>
+__device__ void finalize(const IterArgs& a, const double* S, const double* P) {
+    double H[36], g[6], x[6], sse, cnt;
+    assemble<METRIC>(S, H, g, sse, cnt);
+    const int status = solve6(H, g, cnt, x);
+    double Pn[16];
+    for (int i = 0; i < 16; ++i) Pn[i] = P[i];
+    if (status == CIL_OK) {
+        double dR[9];
+        rodrigues(x, dR);
+        for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 3; ++j)
+                Pn[4 * i + j] = dR[3 * i] * P[j] + dR[3 * i + 1] * P[4 + j] + dR[3 * i + 2] * P[8 + j];
+            Pn[4 * i + 3] = dR[3 * i] * P[3] + dR[3 * i + 1] * P[7] + dR[3 * i + 2] * P[11] + x[3 + i];
+        }
+        Pn[12] = 0.0; Pn[13] = 0.0; Pn[14] = 0.0; Pn[15] = 1.0;
+    }
+    const double rmse = cnt > 0.0 ? sqrt(sse / cnt) : 0.0;
+    if (a.run) {
+        IcpState* st = a.st;
+        const int it = st->iters;
+        if (a.iter_log) { a.iter_log[2 * it] = cnt; a.iter_log[2 * it + 1] = rmse; }
+        st->iters = it + 1;
+        st->n_corr = (long long)cnt;
+        st->rmse = rmse;
+        if (status != CIL_OK) {
+            st->status = status;
+            st->converged = 0;
+            st->done = 1;
+        } else {
+            for (int i = 0; i < 16; ++i) st->pose[i] = Pn[i];
+            const double th = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+            const double tn = sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+            if (th < a.rot_tol && tn < a.trans_tol) { st->converged = 1; st->done = 1; }
+        }
+    } else {
+        for (int i = 0; i < 16; ++i) a.pose_out[i] = Pn[i];
+        if (a.sys) {
+            for (int i = 0; i < 36; ++i) a.sys->H[i] = H[i];
+            for (int i = 0; i < 6; ++i) { a.sys->g[i] = g[i]; a.sys->x[i] = x[i]; }
+            a.sys->sse = sse;
+            a.sys->n_corr = (long long)cnt;
+            a.sys->status = status;
+            a.sys->pad = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- the fused iteration
+template <int METRIC, int B>
+__global__ void __launch_bounds__(kIcpThreads)
+icp_iter_kernel(const IterArgs a) {
+    __shared__ double wsum[kIcpWarps][kSlots];
+    __shared__ double Ssum[kSlots];
+    __shared__ double Psh[16];
+    __shared__ int last;
+    if (a.run && *(volatile int*)&a.st->done) return;
+
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
+    __syncthreads();
+    Pose34 P;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+
+    float acc[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+
+    const TargetView& T = a.T;
+    const unsigned long long none = bound_key(a.bound2);
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += stride) {
+        const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
+        const DF3 s = transform_df(P, px, py, pz);                     // a1
+        unsigned long long best = none;
+        int bpos = -1;
+        if (a.nn_prev) {                                                // warm start: tighter bound
+            const int jp = a.nn_prev[i];
+            if (jp >= 0) offer(s, __ldg(T.pts + jp), jp, best, bpos);
+        }
+        bvh_nearest<B>(T, s, best, bpos);                               // a2
+        const bool acc_ok = best != none;                               // a3
+        if (a.nn_prev) a.nn_prev[i] = acc_ok ? bpos : -1;
+        if (a.corr_idx) a.corr_idx[i] = acc_ok ? (int32_t)key_idx(best) : -1;
+        if (a.corr_d2) a.corr_d2[i] = acc_ok ? key_d2(best) : INFINITY;
+        if (!acc_ok) continue;
+        const float4 t = __ldg(T.pts + bpos);
+        const float dx = dfdiff(s.hx, s.lx, t.x);
+        const float dy = dfdiff(s.hy, s.ly, t.y);
+        const float dz = dfdiff(s.hz, s.lz, t.z);
+        if (METRIC == CIL_POINT_TO_PLANE) {                             // a4 + a5
+            const float4 n = __ldg(T.nrm + bpos);
+            const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
+            const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
+                                fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
+            int k = 0;
+#pragma unroll
+            for (int p = 0; p < 6; ++p)
+#pragma unroll
+                for (int q = p; q < 6; ++q, ++k) acc[k] = fmaf(J[p], J[q], acc[k]);
+#pragma unroll
+            for (int p = 0; p < 6; ++p) acc[21 + p] = fmaf(J[p], r, acc[21 + p]);
+            acc[27] = fmaf(r, r, acc[27]);
+            acc[28] += 1.0f;
+        } else {
+            const float sx = s.hx, sy = s.hy, sz = s.hz;
+            acc[0] += 1.0f;
+            acc[1] += sx; acc[2] += sy; acc[3] += sz;
+            acc[4] = fmaf(sx, sx, acc[4]); acc[5] = fmaf(sy, sy, acc[5]); acc[6] = fmaf(sz, sz, acc[6]);
+            acc[7] = fmaf(sx, sy, acc[7]); acc[8] = fmaf(sx, sz, acc[8]); acc[9] = fmaf(sy, sz, acc[9]);
+            acc[10] += dx; acc[11] += dy; acc[12] += dz;
+            acc[13] += fmaf(sy, dz, -sz * dy);
+            acc[14] += fmaf(sz, dx, -sx * dz);
+            acc[15] += fmaf(sx, dy, -sy * dx);
+            acc[16] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, acc[16])));
+        }
+    }
+
+    // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float mine = warp_transpose_reduce(acc);
+    wsum[warp][lane] = (double)mine;
+    __syncthreads();
+    if (threadIdx.x < kSlots) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
+        a.partials[(size_t)blockIdx.x * kSlots + threadIdx.x] = v;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+
+    // ---- last CTA: ordered fp64 reduction of the per-CTA partials, solve, update
+    __threadfence();
+    {
+        const int k = threadIdx.x & 31, grp = threadIdx.x >> 5;
+        double v = 0.0;
+        for (int b = grp; b < (int)gridDim.x; b += kIcpWarps) v += __ldcg(a.partials + (size_t)b * kSlots + k);
+        wsum[grp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kSlots) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
+        Ssum[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        finalize<METRIC>(a, Ssum, Psh);
+        a.st->ticket = 0;
+    }
+}
+
+// ---------------------------------------------------------------- run bookkeeping kernels
+__global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn_prev, int m,
+                                double* iter_log, int log_len) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid == 0) {
+        for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
+        st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
+        st->done = 0; st->ticket = 0;
+    }
+    for (int i = tid; i < m; i += gridDim.x * blockDim.x) nn_prev[i] = -1;
+    if (iter_log)
+        for (int i = tid; i < log_len; i += gridDim.x * blockDim.x) iter_log[i] = 0.0;
+}
+
+__global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < 16; ++i) res->pose[i] = st->pose[i];
+    res->rmse = st->rmse;
+    res->n_corr = st->n_corr;
+    res->iterations = st->iters;
+    res->converged = st->converged;
+    res->status = st->status;
+    res->pad = 0;
+}
+
+__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; }
+
+template <int METRIC, int B>
+int icp_grid(int m) {
+    static int occ = -1;
+    if (occ < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, icp_iter_kernel<METRIC, B>, kIcpThreads, 0) != cudaSuccess)
+            occ = 1;
+        occ = std::max(occ, 1);
+    }
+    int64_t want = ((int64_t)m + kIcpThreads - 1) / kIcpThreads;
+    int64_t cap = std::min<int64_t>((int64_t)sm_count() * occ, kMaxCtas);
+    return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+template <int METRIC>
+cudaError_t launch_iter_m(const IterArgs& a, int B, cudaStream_t s) {
+    switch (B) {
+        case 4: icp_iter_kernel<METRIC, 4><<<icp_grid<METRIC, 4>(a.m), kIcpThreads, 0, s>>>(a); break;
+        case 8: icp_iter_kernel<METRIC, 8><<<icp_grid<METRIC, 8>(a.m), kIcpThreads, 0, s>>>(a); break;
+        case 16: icp_iter_kernel<METRIC, 16><<<icp_grid<METRIC, 16>(a.m), kIcpThreads, 0, s>>>(a); break;
+        default: icp_iter_kernel<METRIC, 32><<<icp_grid<METRIC, 32>(a.m), kIcpThreads, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
+    count_launches(1);
+    return metric == CIL_POINT_TO_PLANE ? launch_iter_m<CIL_POINT_TO_PLANE>(a, a.T.leaf_size, s)
+                                        : launch_iter_m<CIL_POINT_TO_POINT>(a, a.T.leaf_size, s);
+}
+
+struct WsLayout {
+    size_t state, partials, nn_prev, total;
+};
+
+WsLayout ws_layout(int64_t m) {
+    WsLayout L;
+    L.state = 0;
+    L.partials = 256;
+    L.nn_prev = L.partials + align_up((size_t)kMaxCtas * kSlots * sizeof(double), 256);
+    L.total = L.nn_prev + align_up((size_t)std::max<int64_t>(m, 1) * sizeof(int), 256);
+    return L;
+}
+
+cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
+                        void* ws, size_t ws_bytes) {
+    if (!t || !p) { set_error("%s: NULL target or params", fn); return CIL_ERR_INVALID_ARG; }
+    if (m < 0 || m > INT32_MAX) { set_error("%s: m=%lld out of range", fn, (long long)m); return CIL_ERR_INVALID_ARG; }
+    if (m > 0 && !src) { set_error("%s: src is NULL", fn); return CIL_ERR_INVALID_ARG; }
+    if (p->metric != CIL_POINT_TO_POINT && p->metric != CIL_POINT_TO_PLANE) {
+        set_error("%s: metric %d not supported", fn, p->metric);
+        return CIL_ERR_INVALID_ARG;
+    }
+    if (!(p->max_corr_dist > 0.0)) { set_error("%s: max_corr_dist must be > 0", fn); return CIL_ERR_INVALID_ARG; }
+    if (!(p->rot_tol >= 0.0) || !(p->trans_tol >= 0.0)) { set_error("%s: tolerances must be >= 0", fn); return CIL_ERR_INVALID_ARG; }
+    if (p->w_point != 0.0 || p->w_plane != 0.0) { set_error("%s: w_point/w_plane are reserved (0)", fn); return CIL_ERR_INVALID_ARG; }
+    if (p->metric == CIL_POINT_TO_PLANE && !t->has_normals) {
+        set_error("%s: point-to-plane needs a target built with normals", fn);
+        return CIL_ERR_NO_NORMALS;
+    }
+    if (!ws || ((uintptr_t)ws & 255u)) { set_error("%s: workspace NULL or not 256-B aligned", fn); return CIL_ERR_WORKSPACE; }
+    if (ws_bytes < ws_layout(m).total) {
+        set_error("%s: workspace %zu B < required %zu B", fn, ws_bytes, ws_layout(m).total);
+        return CIL_ERR_WORKSPACE;
+    }
+    return CIL_OK;
+}
+
+float bound2_of(double max_dist) {
+    return std::isinf(max_dist) ? INFINITY : (float)(max_dist * max_dist);
+}
+
+}  // namespace
+}  // namespace cil
+
+using namespace cil;
+
+CIL_API size_t cil_icp_workspace_bytes(int64_t m, const cil_icp_params* params) {
+    (void)params;
+    if (m < 0 || m > INT32_MAX) return 0;
+    return ws_layout(m).total;
+}
+
+CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_t m, const double* pose_in,
+                                   const cil_icp_params* params, void* ws, size_t ws_bytes, double* pose_out,
+                                   cil_icp_system* sys, int32_t* corr_idx, float* corr_sqdist, cil_stream_t stream) {
+    cil_status rc = check_common("cil_icp_iterate", t, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_in || !pose_out) { set_error("cil_icp_iterate: pose_in/pose_out NULL"); return CIL_ERR_INVALID_ARG; }
+    const WsLayout L = ws_layout(m);
+    char* w = (char*)ws;
+    IterArgs a{};
+    a.T = t->v;
+    a.src = src;
+    a.m = (int)m;
+    a.bound2 = bound2_of(params->max_corr_dist);
+    a.pose_in = pose_in;
+    a.pose_out = pose_out;
+    a.partials = (double*)(w + L.partials);
+    a.st = (IcpState*)(w + L.state);
+    a.sys = sys;
+    a.corr_idx = corr_idx;
+    a.corr_d2 = corr_sqdist;
+    a.nn_prev = nullptr;
+    a.iter_log = nullptr;
+    a.run = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
+    count_launches(1);
+    cudaError_t e = launch_iter(a, params->metric, s);
+    if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                               const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                               double* iter_log, cil_stream_t stream) {
+    cil_status rc = check_common("cil_icp_run", t, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_init || !res) { set_error("cil_icp_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
+    if (params->max_iters < 1) { set_error("cil_icp_run: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
+    const WsLayout L = ws_layout(m);
+    char* w = (char*)ws;
+    IterArgs a{};
+    a.T = t->v;
+    a.src = src;
+    a.m = (int)m;
+    a.bound2 = bound2_of(params->max_corr_dist);
+    a.st = (IcpState*)(w + L.state);
+    a.pose_in = a.st->pose;
+    a.pose_out = a.st->pose;
+    a.partials = (double*)(w + L.partials);
+    a.nn_prev = (int*)(w + L.nn_prev);
+    a.iter_log = iter_log;
+    a.run = 1;
+    a.rot_tol = params->rot_tol;
+    a.trans_tol = params->trans_tol;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn_prev, (int)m, iter_log, 2 * params->max_iters);
+    count_launches(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
+    for (int it = 0; it < params->max_iters; ++it) {
+        e = launch_iter(a, params->metric, s);
+        if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
+    }
+    run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
+    count_launches(1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
+    return CIL_OK;
+}

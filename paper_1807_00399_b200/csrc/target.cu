@@ -1,0 +1,351 @@
+// target.cu -- cil_target_build: the GPU spatial index over the target cloud
+// (BASELINE.json north_star subsystem (2): "a GPU spatial index over
+// the target, such as ... Morton-sorted cells built by a device radix sort plus a
+// cell-offset scan ... chosen by measurement").
+//
+// Pipeline (all hand-written kernels, one stream, no host synchronisation):
+//   K1a bbox partials -> K1b bbox final -> K1c 48-bit Morton key per point
+//   K2  stable LSD radix sort of (key, index) (6 passes x 8 bits: histogram, scan, scatter)
+//   K4  gather: sorted float4 (x, y, z, orig index) points and float4 normals
+//   K5  leaf AABBs (leaf_size consecutive sorted points), then internal AABBs level by level
+//       of an implicit complete binary tree (node v has children 2v, 2v+1).
+#include "internal.cuh"
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+namespace cil {
+namespace {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ bbox
+__global__ void bbox_partial_kernel(const float* __restrict__ p, int n, float* __restrict__ part) {
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float c = p[3 * (size_t)i + a];
+            mn[a] = fminf(mn[a], c);
+            mx[a] = fmaxf(mx[a], c);
+        }
+    }
+    __shared__ float s[6][kThreads / 32];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { s[a][w] = mn[a]; s[3 + a][w] = mx[a]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[threadIdx.x][0];
+        for (int k = 1; k < kThreads / 32; ++k)
+            v = threadIdx.x < 3 ? fminf(v, s[threadIdx.x][k]) : fmaxf(v, s[threadIdx.x][k]);
+        part[6 * blockIdx.x + threadIdx.x] = v;
+    }
+}
+
+// bbox[0..2] = min, bbox[3] = scale (cells per unit), bbox[4..5] unused
+__global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, float* __restrict__ bbox) {
+    if (threadIdx.x != 0) return;
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int b = 0; b < nblk; ++b)
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = fminf(mn[a], part[6 * b + a]);
+            mx[a] = fmaxf(mx[a], part[6 * b + 3 + a]);
+        }
+    float ext = fmaxf(fmaxf(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
+    float cells = (float)((1 << kMortonBits) - 1);
+    bbox[0] = mn[0]; bbox[1] = mn[1]; bbox[2] = mn[2];
+    bbox[3] = ext > 0.0f ? cells / ext : 0.0f;
+}
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {
+    // 16 bits -> every third bit of a 48-bit word
+    x &= 0xffffull;
+    x = (x | (x << 16)) & 0x0000ff0000ffull;
+    x = (x | (x << 8)) & 0x00f00f00f00full;
+    x = (x | (x << 4)) & 0x0c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x249249249249ull;
+    return x;
+}
+
+__global__ void morton_kernel(const float* __restrict__ p, int n, const float* __restrict__ bbox,
+                              unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const float mx = bbox[0], my = bbox[1], mz = bbox[2], sc = bbox[3];
+    const float cmax = (float)((1 << kMortonBits) - 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        float x = p[3 * (size_t)i], y = p[3 * (size_t)i + 1], z = p[3 * (size_t)i + 2];
+        unsigned qx = (unsigned)fminf(fmaxf((x - mx) * sc, 0.0f), cmax);
+        unsigned qy = (unsigned)fminf(fmaxf((y - my) * sc, 0.0f), cmax);
+        unsigned qz = (unsigned)fminf(fmaxf((z - mz) * sc, 0.0f), cmax);
+        keys[i] = (spread3(qx) << 2) | (spread3(qy) << 1) | spread3(qz);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// ------------------------------------------------------------------ radix sort (stable LSD)
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortWarps = kThreads / 32;
+constexpr int kItemsPerWarp = 512;                       // 16 rounds of 32
+constexpr int kTile = kSortWarps * kItemsPerWarp;         // 4096 keys per block
+
+__device__ __forceinline__ int digit_of(unsigned long long k, int shift) { return (int)((k >> shift) & (kRadix - 1)); }
+
+// hist[d * nblk + b] = number of keys with digit d in tile b
+__global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, int n, int shift,
+                                  uint32_t* __restrict__ hist, int nblk) {
+    __shared__ uint32_t h[kRadix];
+    for (int d = threadIdx.x; d < kRadix; d += blockDim.x) h[d] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * kTile;
+    for (int i = threadIdx.x; i < kTile; i += blockDim.x) {
+        int g = base + i;
+        if (g < n) atomicAdd(&h[digit_of(keys[g], shift)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(size_t)d * nblk + blockIdx.x] = h[d];
+}
+
+// in-place exclusive scan of `len` counters with one block of 1024 threads
+__global__ void scan_kernel(uint32_t* __restrict__ a, int len) {
+    __shared__ uint32_t part[1024];
+    const int t = threadIdx.x;
+    const int per = (len + 1023) / 1024;
+    const int beg = t * per, end = min(beg + per, len);
+    uint32_t s = 0;
+    for (int i = beg; i < end; ++i) s += a[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        uint32_t v = t >= o ? part[t - o] : 0u;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[t] - s;   // exclusive prefix of this thread's chunk
+    for (int i = beg; i < end; ++i) {
+        uint32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+}
+
+// stable scatter: within a tile, warp w owns keys [w*512, (w+1)*512) processed in rounds of 32
+__global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                     unsigned long long* __restrict__ kout, uint32_t* __restrict__ vout,
+                                     int n, int shift, const uint32_t* __restrict__ offs, int nblk) {
+    __shared__ uint32_t cnt[kSortWarps][kRadix];   // per-warp digit counts, then offsets
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int d = l; d < kRadix; d += 32) cnt[w][d] = 0;
+    __syncwarp();
+    const int wbase = blockIdx.x * kTile + w * kItemsPerWarp;
+    const unsigned lt_mask = (1u << l) - 1u;
+    // pass 1: per-warp digit histogram
+    for (int r = 0; r < kItemsPerWarp; r += 32) {
+        int g = wbase + r + l;
+        bool ok = g < n;
+        int d = ok ? digit_of(kin[g], shift) : -1;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (ok && (peers & lt_mask) == 0) cnt[w][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // offsets: global base of (digit, tile) + counts of lower warps in this tile
+    for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
+        uint32_t run = offs[(size_t)d * nblk + blockIdx.x];
+        for (int k = 0; k < kSortWarps; ++k) {
+            uint32_t c = cnt[k][d];
+            cnt[k][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // pass 2: scatter in position order
+    for (int r = 0; r < kItemsPerWarp; r += 32) {
+        int g = wbase + r + l;
+        bool ok = g < n;
+        unsigned long long k = ok ? kin[g] : 0ull;
+        int d = ok ? digit_of(k, shift) : -1;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (ok) {
+            uint32_t dst = cnt[w][d] + __popc(peers & lt_mask);
+            kout[dst] = k;
+            vout[dst] = vin[g];
+        }
+        __syncwarp();
+        if (ok && (peers & lt_mask) == 0) cnt[w][d] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ gather + tree
+__global__ void gather_kernel(const float* __restrict__ p, const float* __restrict__ nrm, int n,
+                              const uint32_t* __restrict__ perm, float4* __restrict__ pts, float4* __restrict__ nout) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t o = perm[i];
+        pts[i] = make_float4(p[3 * (size_t)o], p[3 * (size_t)o + 1], p[3 * (size_t)o + 2], __int_as_float((int)o));
+        if (nout) nout[i] = make_float4(nrm[3 * (size_t)o], nrm[3 * (size_t)o + 1], nrm[3 * (size_t)o + 2], 0.0f);
+    }
+}
+
+__global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, int l_pad, float4* __restrict__ box) {
+    for (int leaf = blockIdx.x * blockDim.x + threadIdx.x; leaf < l_pad; leaf += gridDim.x * blockDim.x) {
+        float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f);
+        float4 hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
+        const int beg = leaf * B, end = min(beg + B, n);
+        for (int j = beg; j < end; ++j) {
+            float4 t = pts[j];
+            lo.x = fminf(lo.x, t.x); lo.y = fminf(lo.y, t.y); lo.z = fminf(lo.z, t.z);
+            hi.x = fmaxf(hi.x, t.x); hi.y = fmaxf(hi.y, t.y); hi.z = fmaxf(hi.z, t.z);
+        }
+        const size_t v = (size_t)l_pad + leaf;
+        box[2 * v] = lo;
+        box[2 * v + 1] = hi;
+    }
+}
+
+// nodes [first, 2*first) from their children
+__global__ void level_box_kernel(float4* __restrict__ box, int first) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < first; k += gridDim.x * blockDim.x) {
+        const size_t v = (size_t)first + k, c = 2 * v;
+        float4 l0 = box[2 * c], h0 = box[2 * c + 1], l1 = box[2 * c + 2], h1 = box[2 * c + 3];
+        box[2 * v] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.0f);
+        box[2 * v + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.0f);
+    }
+}
+
+inline int grid_for(int64_t work, int threads = kThreads) {
+    int64_t b = (work + threads - 1) / threads;
+    int cap = sm_count() * 8;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+}  // namespace
+}  // namespace cil
+
+using namespace cil;
+
+CIL_API cil_status cil_target_build(const float* pts, const float* normals, int64_t n,
+                                    const cil_index_params* params, cil_stream_t stream, cil_target** out) {
+    if (!out) { set_error("cil_target_build: out is NULL"); return CIL_ERR_INVALID_ARG; }
+    *out = nullptr;
+    if (n == 0) { set_error("cil_target_build: empty target (n == 0)"); return CIL_ERR_EMPTY_TARGET; }
+    if (n < 0 || n > INT32_MAX) { set_error("cil_target_build: n=%lld out of range", (long long)n); return CIL_ERR_INVALID_ARG; }
+    if (!pts) { set_error("cil_target_build: pts is NULL"); return CIL_ERR_INVALID_ARG; }
+    int B = 8;
+    if (params) {
+        if (params->leaf_size) B = params->leaf_size;
+        for (int k = 0; k < 7; ++k)
+            if (params->reserved[k]) { set_error("cil_target_build: reserved index params must be 0"); return CIL_ERR_INVALID_ARG; }
+    }
+    if (B != 4 && B != 8 && B != 16 && B != 32) {
+        set_error("cil_target_build: leaf_size %d not in {4, 8, 16, 32}", B);
+        return CIL_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int N = (int)n;
+    const int64_t n_leaves = (N + B - 1) / B;
+    int64_t l_pad = 1;
+    while (l_pad < n_leaves) l_pad <<= 1;
+
+    // one allocation: pts (16N), nrm (16N), box (2 * 2*l_pad * 16)
+    const size_t b_pts = align_up((size_t)N * 16, 256);
+    const size_t b_nrm = normals ? align_up((size_t)N * 16, 256) : 0;
+    const size_t b_box = align_up((size_t)4 * l_pad * 16, 256);
+    const size_t bytes = b_pts + b_nrm + b_box;
+    int dev = 0;
+    CIL_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    void* mem = nullptr;
+    CIL_CUDA_TRY(cudaMallocAsync(&mem, bytes, s), "cudaMallocAsync(target)");
+    char* base = (char*)mem;
+    float4* d_pts = (float4*)base;
+    float4* d_nrm = normals ? (float4*)(base + b_pts) : nullptr;
+    float4* d_box = (float4*)(base + b_pts + b_nrm);
+
+    // scratch: keys x2 (8N), vals x2 (4N), hist (256 * nblk), bbox partials
+    const int nblk_sort = (N + kTile - 1) / kTile;
+    const int nblk_bbox = grid_for(N);
+    const size_t s_keys = align_up((size_t)N * 8, 256), s_vals = align_up((size_t)N * 4, 256);
+    const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
+    const size_t s_bb = align_up((size_t)(6 * nblk_bbox + 8) * 4, 256);
+    const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb;
+    void* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, scratch, s);
+    if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cudaMallocAsync(scratch)"); }
+    char* tb = (char*)tmp;
+    unsigned long long* k0 = (unsigned long long*)tb;
+    unsigned long long* k1 = (unsigned long long*)(tb + s_keys);
+    uint32_t* v0 = (uint32_t*)(tb + 2 * s_keys);
+    uint32_t* v1 = (uint32_t*)(tb + 2 * s_keys + s_vals);
+    uint32_t* hist = (uint32_t*)(tb + 2 * s_keys + 2 * s_vals);
+    float* bbp = (float*)(tb + 2 * s_keys + 2 * s_vals + s_hist);
+    float* bbox = bbp + 6 * nblk_bbox;
+
+    bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, N, bbp);
+    bbox_final_kernel<<<1, 32, 0, s>>>(bbp, nblk_bbox, bbox);
+    morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, bbox, k0, v0);
+    for (int shift = 0; shift < 3 * kMortonBits; shift += kRadixBits) {
+        radix_hist_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, N, shift, hist, nblk_sort);
+        scan_kernel<<<1, 1024, 0, s>>>(hist, kRadix * nblk_sort);
+        radix_scatter_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, v0, k1, v1, N, shift, hist, nblk_sort);
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+    }
+    gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, d_pts, d_nrm);
+    leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(d_pts, N, B, (int)l_pad, d_box);
+    for (int64_t first = l_pad / 2; first >= 1; first /= 2)
+        level_box_kernel<<<grid_for(first), kThreads, 0, s>>>(d_box, (int)first);
+    {
+        int levels = 0;
+        for (int64_t f = l_pad / 2; f >= 1; f /= 2) ++levels;
+        count_launches(3 + 3 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + 2 + levels);
+    }
+    e = cudaGetLastError();
+    cudaFreeAsync(tmp, s);
+    if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cil_target_build launch"); }
+
+    cil_target* t = new cil_target;
+    t->v.pts = d_pts;
+    t->v.nrm = d_nrm;
+    t->v.box = d_box;
+    t->v.n = N;
+    t->v.l_pad = (int)l_pad;
+    t->v.leaf_size = B;
+    t->n_leaves = n_leaves;
+    t->has_normals = normals ? 1 : 0;
+    t->device = dev;
+    t->mem = mem;
+    t->bytes = bytes;
+    *out = t;
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_target_free(cil_target* t, cil_stream_t stream) {
+    if (!t) return CIL_OK;
+    cudaError_t e = cudaFreeAsync(t->mem, (cudaStream_t)stream);
+    delete t;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(target)");
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_target_get_info(const cil_target* t, cil_target_info* info) {
+    if (!t || !info) { set_error("cil_target_get_info: NULL argument"); return CIL_ERR_INVALID_ARG; }
+    info->n = t->v.n;
+    info->n_leaves = t->n_leaves;
+    info->n_nodes = 2 * (int64_t)t->v.l_pad;
+    info->leaf_size = t->v.leaf_size;
+    info->has_normals = t->has_normals;
+    info->device_bytes = (int64_t)t->bytes;
+    return CIL_OK;
+}

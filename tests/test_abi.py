@@ -1,0 +1,105 @@
+"""CPU-side checks of the C ABI boundary (no GPU needed): libcil.so loads, exports every
+function include/cil.h declares, the ctypes struct layouts equal the C layouts, and the
+host-detectable argument errors are returned before anything touches the device."""
+import ctypes as C
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "cil.h")
+
+
+def _declared_functions():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cil_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def cil():
+    import paper_1807_00399_b200 as cil
+    return cil
+
+
+def test_library_exports_every_declared_symbol(cil):
+    names = _declared_functions()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(cil.lib(), n), f"libcil.so does not export {n}"
+    assert sorted(cil.EXPORTED) == names
+    assert "sm_100a" in cil.version()
+
+
+def test_struct_layouts_match_header(cil):
+    """Compile a probe against include/cil.h and compare sizeof/offsetof with ctypes."""
+    probe = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "cil.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu\n", sizeof(cil_index_params), sizeof(cil_icp_params), sizeof(cil_icp_result),
+         sizeof(cil_icp_system), sizeof(cil_target_info));
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(cil_icp_params, max_corr_dist), offsetof(cil_icp_result, rmse),
+         offsetof(cil_icp_result, status), offsetof(cil_icp_system, sse), offsetof(cil_icp_system, status),
+         offsetof(cil_target_info, device_bytes));
+  return 0;
+}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "p.c")
+        exe = os.path.join(d, "p")
+        open(c, "w").write(probe)
+        subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+        out = subprocess.check_output([exe]).decode().split()
+    sizes = [int(x) for x in out[:5]]
+    offs = [int(x) for x in out[5:]]
+    assert sizes == [C.sizeof(cil.cil_index_params), C.sizeof(cil.cil_icp_params), C.sizeof(cil.cil_icp_result),
+                     C.sizeof(cil.cil_icp_system), C.sizeof(cil.cil_target_info)]
+    assert offs == [cil.cil_icp_params.max_corr_dist.offset, cil.cil_icp_result.rmse.offset,
+                    cil.cil_icp_result.status.offset, cil.cil_icp_system.sse.offset,
+                    cil.cil_icp_system.status.offset, cil.cil_target_info.device_bytes.offset]
+
+
+def test_host_side_argument_errors(cil):
+    L = cil.lib()
+    h = C.c_void_p()
+    assert L.cil_target_build(None, None, 0, None, None, C.byref(h)) == cil.CIL_ERR_EMPTY_TARGET
+    assert L.cil_target_build(None, None, -5, None, None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_target_build(None, None, 10, None, None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_target_build(None, None, 2 ** 31, None, None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_target_build(None, None, 10, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    bad = cil.cil_index_params()
+    bad.leaf_size = 7
+    assert L.cil_target_build(C.c_void_p(256), None, 10, C.byref(bad), None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+    assert "leaf_size" in L.cil_last_error().decode()
+    assert L.cil_nn_query(None, None, 10, 1.0, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    p = cil.make_params("point_to_plane", 10, 0.1)
+    assert L.cil_icp_iterate(None, None, 10, None, C.byref(p), None, 0, None, None, None, None, None) == \
+        cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_run(None, None, 10, None, C.byref(p), None, 0, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_target_free(None, None) == cil.CIL_OK
+    assert L.cil_status_string(cil.CIL_ERR_DEGENERATE) == b"CIL_ERR_DEGENERATE"
+
+
+def test_workspace_bytes_host_only(cil):
+    p = cil.make_params("point_to_plane", 50, 1.0)
+    a = cil.cil_icp_workspace_bytes(1000, p)
+    b = cil.cil_icp_workspace_bytes(2_000_000, p)
+    assert a > 0 and b > a and a % 256 == 0 and b % 256 == 0
+    assert b - a >= 4 * (2_000_000 - 1000) - 256     # per-point warm-start state
+    assert cil.cil_icp_workspace_bytes(-1, p) == 0
+    assert cil.cil_icp_workspace_bytes(2 ** 31, p) == 0
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports or links the oracle (boundary)."""
+    pkg = os.path.join(ROOT, "paper_1807_00399_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "liboracle" not in txt and "orc_" not in txt, f

@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same
+seeded inputs.  Tolerances are BASELINE.json north_star's:
+  * NN indices bit-exact wherever (d2_2nd - d2_best) > 1e-6 * d2_best (else the GPU's pick
+    must itself be within the near-tie band), NN d^2 within 1e-6 relative;
+  * rejection decisions equal outside the ambiguous band |d^2/max^2 - 1| <= 2e-6 (R2);
+  * H within 1e-5 relative Frobenius, g within 1e-5 of ||g|| (or of ||sum|J r|||, R16),
+    also after reconciling near-tie flips through the GPU's own correspondences (R17);
+  * final poses within 1e-4 rad and 1e-5 units.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from tests import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+NN_REL = 1e-6
+BAND = 2e-6
+
+
+@pytest.fixture(scope="module")
+def cil():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1807_00399_b200 as cil
+    return cil
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def check_nn(tgt, queries_f64, g_idx, g_d2, o_idx, o_d2, max_d2=math.inf):
+    """GPU NN (g_*) vs oracle k=2 NN (o_* [m,2]) with the north_star masks."""
+    g_idx = np.asarray(g_idx, np.int64)
+    g_d2 = np.asarray(g_d2, np.float64)
+    d1, d2nd = o_d2[:, 0], o_d2[:, 1]
+    o_acc = o_idx[:, 0] >= 0
+    g_acc = g_idx >= 0
+    band = np.isfinite(max_d2) & (np.abs(d1 / max_d2 - 1.0) <= BAND) if np.isfinite(max_d2) else np.zeros(len(d1), bool)
+    mism = (o_acc != g_acc) & ~band
+    assert not mism.any(), f"{mism.sum()} rejection decisions differ outside the band"
+    both = o_acc & g_acc
+    # distances within 1e-6 relative (exact zero stays zero)
+    err = np.abs(g_d2[both] - d1[both])
+    assert (err <= NN_REL * d1[both]).all(), f"max rel d2 err {np.max(err / np.maximum(d1[both], 1e-300))}"
+    # indices bit-exact outside the near-tie band
+    with np.errstate(invalid="ignore"):
+        clear = both & ~(d2nd - d1 <= NN_REL * d1)      # inf - inf (no 2nd point) counts as clear
+    bad = clear & (g_idx != o_idx[:, 0])
+    assert not bad.any(), f"{bad.sum()} NN indices differ with a clear gap"
+    # inside the band the GPU's pick must itself be a near-tie (fp64 distance of its pick)
+    tie = both & ~clear & (g_idx != o_idx[:, 0])
+    if tie.any():
+        q = queries_f64[tie]
+        t = tgt[g_idx[tie]].astype(np.float64)
+        dd = ((q - t) ** 2).sum(1)
+        assert (dd <= d1[tie] * (1 + 2 * NN_REL) + 0.0).all()
+    return int(clear.sum()), int(tie.sum())
+
+
+# ------------------------------------------------------------------ NN
+@pytest.mark.parametrize("n,m,leaf", [(1, 5, 8), (7, 33, 8), (8, 64, 8), (9, 257, 4), (1000, 1000, 16),
+                                      (4097, 3001, 32), (65537, 100003, 8)])
+def test_nn_small_ragged(cil, n, m, leaf):
+    rng = np.random.default_rng(n + m)
+    T = rng.standard_normal((n, 3)).astype(np.float32)
+    Q = (rng.standard_normal((m, 3)) * 1.1).astype(np.float32)
+    t = cil.cil_target_build(dev(T), None, leaf_size=leaf)
+    gi, gd = cil.cil_nn_query(t, dev(Q))
+    o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2)
+    check_nn(T, Q.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2)
+    info = t.info()
+    assert info.n == n and info.leaf_size == leaf and info.n_leaves == (n + leaf - 1) // leaf
+
+
+def test_nn_ties_lowest_original_index(cil):
+    """R1: exact ties (duplicated integer grid points, cube centres) -> lowest original index."""
+    g = np.stack(np.meshgrid(*[np.arange(10)] * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.float32)
+    T = np.concatenate([g[::-1], g, g[::-1]])
+    Q = np.concatenate([g, g + 0.5, g + 0.25, g - 0.5]).astype(np.float32)
+    t = cil.cil_target_build(dev(T), None, leaf_size=4)
+    gi, gd = cil.cil_nn_query(t, dev(Q))
+    from scipy.spatial.distance import cdist
+    D = cdist(Q.astype(np.float64), T.astype(np.float64), "sqeuclidean")
+    ref = np.argmin(D, 1)
+    assert np.array_equal(gi.cpu().numpy(), ref)
+    assert np.array_equal(gd.cpu().numpy().astype(np.float64), D[np.arange(len(Q)), ref])
+
+
+def test_nn_bounded_and_empty(cil):
+    rng = np.random.default_rng(1)
+    T = rng.random((5000, 3)).astype(np.float32)
+    Q = rng.random((7000, 3)).astype(np.float32)
+    t = cil.cil_target_build(dev(T), None)
+    for md in (0.0, 0.01, 0.03):
+        gi, gd = cil.cil_nn_query(t, dev(Q), max_dist=md)
+        o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2, max_dist=md)
+        check_nn(T, Q.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2,
+                 max_d2=float(np.float32(md) ** 2) if md > 0 else 0.0)
+    # empty query set
+    gi, gd = cil.cil_nn_query(t, torch.empty((0, 3), device="cuda"))
+    assert gi.numel() == 0
+    # self query -> itself at distance 0
+    gi, gd = cil.cil_nn_query(t, dev(T))
+    assert np.array_equal(gi.cpu().numpy(), np.arange(5000)) and (gd.cpu().numpy() == 0).all()
+
+
+def test_nn_c2_full_size(cil):
+    """BASELINE.json configs[1] at full size (2^20 x 2^20), every query checked."""
+    w = W.c2()
+    t = cil.cil_target_build(dev(w.target), None)
+    gi, gd = cil.cil_nn_query(t, dev(w.source))
+    torch.cuda.synchronize()
+    o_idx, o_d2 = oracle.knn(None, w.source.astype(np.float64), k=2, tree=W.oracle_tree(w))
+    clear, tie = check_nn(w.target, w.source.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2)
+    assert clear >= w.m - 50
+
+
+# ------------------------------------------------------------------ one iteration
+def _pose(R=np.eye(3), t=np.zeros(3)):
+    T = np.eye(4)
+    T[:3, :3] = R
+    T[:3, 3] = t
+    return T
+
+
+def _perturb(gt, frac):
+    """pose `frac` of the way from identity to ground truth"""
+    from scipy.spatial.transform import Rotation
+    rv = Rotation.from_matrix(gt[:3, :3]).as_rotvec() * frac
+    return _pose(Rotation.from_rotvec(rv).as_matrix(), gt[:3, 3] * frac)
+
+
+def check_iteration(cil, w, pose, metric, tree=None, sample=None, leaf=0):
+    """cil_icp_iterate vs oracle at the same pose_in: correspondences, H, g, pose_out."""
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals) if w.target_normals is not None else None,
+                             leaf_size=leaf)
+    prm = cil.make_params(metric, 1, w.max_dist)
+    P = dev(pose.astype(np.float64))
+    pose_out, sys_t, ci, cd = cil.cil_icp_iterate(t, dev(w.source), P, prm, want_corr=True)
+    gs = cil.decode_system(sys_t)
+    g_idx = ci.cpu().numpy()
+    g_d2 = cd.cpu().numpy()
+    tree = tree or W.oracle_tree(w)
+    o = oracle.icp_system(None, w.target_normals, w.source, pose, metric, w.max_dist, tree=tree)
+    s64 = oracle.transform(pose, w.source)
+    o_idx = np.stack([o.corr_idx, np.where(np.isfinite(o.corr_d2nd), 0, -1)], 1)
+    o_d2 = np.stack([o.corr_d2, o.corr_d2nd], 1)
+    check_nn(w.target, s64, g_idx, g_d2, o_idx, o_d2, max_d2=w.max_dist ** 2)
+    # H, g against the oracle's own system (R16) ...
+    assert gs.status == cil.CIL_OK
+    assert abs(gs.n_corr - o.count) <= max(2, 1e-5 * o.count)
+    relH = np.linalg.norm(gs.H - o.H) / np.linalg.norm(o.H)
+    gscale = max(np.linalg.norm(o.g), 1e-3 * np.linalg.norm(o.gabs))
+    relg = np.linalg.norm(gs.g - o.g) / gscale
+    assert relH <= 1e-5 and relg <= 1e-5, (relH, relg)
+    # ... and reconciled through the GPU's own correspondences (R17): much tighter
+    r = oracle.icp_system_from_corr(w.target, w.target_normals, w.source, pose, metric, g_idx.astype(np.int32))
+    assert r.count == gs.n_corr
+    relH2 = np.linalg.norm(gs.H - r.H) / np.linalg.norm(r.H)
+    relg2 = np.linalg.norm(gs.g - r.g) / max(np.linalg.norm(r.g), 1e-3 * np.linalg.norm(r.gabs))
+    assert relH2 <= 1e-6 and relg2 <= 1e-5, (relH2, relg2)
+    # pose_out: the oracle's solve/update of the GPU's own (H, g) ...
+    st, Pr, x, _, _ = oracle.solve_update(gs.H, gs.g, gs.n_corr, pose)
+    Pg = pose_out.cpu().numpy()
+    assert W.rot_angle(Pg[:3, :3] @ Pr[:3, :3].T) < 1e-12 and np.abs(Pg[:3, 3] - Pr[:3, 3]).max() < 1e-12
+    # ... and the oracle's full step
+    st, Po, *_ = oracle.solve_update(o.H, o.g, o.count, pose)
+    assert W.rot_angle(Pg[:3, :3] @ Po[:3, :3].T) < 1e-4 and np.abs(Pg[:3, 3] - Po[:3, 3]).max() < 1e-5
+    return gs, g_idx
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.7])
+def test_iterate_c1(cil, frac):
+    w = W.c1()
+    check_iteration(cil, w, _perturb(w.gt_pose, frac), "point_to_plane")
+
+
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+def test_iterate_c4_reduced(cil, metric):
+    w = W.c4(metric, rings=16, az=8000)
+    for frac in (0.0, 0.5, 1.0):
+        check_iteration(cil, w, _perturb(w.gt_pose, frac), metric)
+
+
+@pytest.mark.parametrize("logn", [16, 18])
+def test_iterate_c5(cil, logn):
+    w = W.c5(logn)
+    check_iteration(cil, w, np.eye(4), "point_to_plane")
+
+
+def test_iterate_c3(cil):
+    w = W.c3()
+    check_iteration(cil, w, np.eye(4), "point_to_plane")
+
+
+@pytest.mark.parametrize("leaf", [4, 16, 32])
+def test_iterate_leaf_sizes(cil, leaf):
+    w = W.c4("point_to_plane", rings=8, az=6000)
+    check_iteration(cil, w, _perturb(w.gt_pose, 0.3), "point_to_plane", leaf=leaf)
+
+
+# ------------------------------------------------------------------ the loop
+def check_run(cil, w, metric, leaf=0):
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals) if w.target_normals is not None else None,
+                             leaf_size=leaf)
+    prm = cil.make_params(metric, w.max_iters, w.max_dist)
+    res_t, log = cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)
+    res = cil.decode_result(res_t)
+    o = oracle.icp_run(None, w.target_normals, w.source, metric, w.max_iters, w.max_dist, tree=W.oracle_tree(w))
+    assert res.status == o.status == cil.CIL_OK
+    assert res.iterations == o.iterations == w.max_iters
+    dr = W.rot_angle(res.pose[:3, :3] @ o.pose[:3, :3].T)
+    dt = np.abs(res.pose[:3, 3] - o.pose[:3, 3]).max()
+    assert dr <= 1e-4 and dt <= 1e-5, (dr, dt)
+    lg = log.cpu().numpy()
+    np.testing.assert_allclose(lg[:, 0], o.iter_log[:, 0], rtol=1e-4, atol=3)
+    # rmse: a near-tie or rejection-band flip swaps a pair's plane residual outright, so the
+    # per-iteration rmse agrees to ~1e-4 relative, not to the pose tolerance
+    np.testing.assert_allclose(lg[:, 1], o.iter_log[:, 1], rtol=1e-3)
+    # the loop equals the chain of stateless iterations bit for bit (warm start is exact)
+    P = dev(np.eye(4))
+    for _ in range(w.max_iters):
+        P, *_ = cil.cil_icp_iterate(t, dev(w.source), P, prm, want_sys=False)
+    assert np.array_equal(P.cpu().numpy(), res.pose)
+    return res, o
+
+
+def test_run_c1(cil):
+    check_run(cil, W.c1(), "point_to_plane")
+
+
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+def test_run_c4_reduced(cil, metric):
+    check_run(cil, W.c4(metric, rings=16, az=8000), metric)
+
+
+def test_run_c3(cil):
+    check_run(cil, W.c3(), "point_to_plane")
+
+
+# ------------------------------------------------------------------ statuses and edge cases
+def test_status_degenerate_no_corr_and_alias(cil):
+    rng = np.random.default_rng(4)
+    pts = rng.uniform(-1, 1, (500, 3)).astype(np.float32)
+    pts[:, 2] = 0
+    nrm = np.tile(np.array([[0, 0, 1]], np.float32), (500, 1))
+    t = cil.cil_target_build(dev(pts), dev(nrm))
+    prm = cil.make_params("point_to_plane", 5, 0.1)
+    res_t, _ = cil.cil_icp_run(t, dev(pts + np.float32(0.01)), dev(np.eye(4)), prm)
+    res = cil.decode_result(res_t)
+    assert res.status == cil.CIL_ERR_DEGENERATE and not res.converged and res.iterations == 1
+    assert np.array_equal(res.pose, np.eye(4))
+    res_t, _ = cil.cil_icp_run(t, dev(pts + np.float32(100)), dev(np.eye(4)), prm)
+    res = cil.decode_result(res_t)
+    assert res.status == cil.CIL_NO_CORRESPONDENCES and res.n_corr == 0 and res.iterations == 1
+    # in-place iterate (pose_in aliases pose_out), m == 0 -> no correspondences, pose kept
+    P = dev(np.eye(4))
+    P2, sys_t, _, _ = cil.cil_icp_iterate(t, torch.empty((0, 3), device="cuda"), P, prm, pose_out=P)
+    assert cil.decode_system(sys_t).status == cil.CIL_NO_CORRESPONDENCES
+    assert np.array_equal(P.cpu().numpy(), np.eye(4))
+    # point-to-plane without normals is a host-side error
+    t2 = cil.cil_target_build(dev(pts), None)
+    with pytest.raises(cil.CilError) as e:
+        cil.cil_icp_iterate(t2, dev(pts), P, prm)
+    assert e.value.status == cil.CIL_ERR_NO_NORMALS
+
+
+def test_converges_and_stops(cil):
+    """tgt = src with tolerances -> converged after 1 iteration; later launches do nothing."""
+    w = W.c4("point_to_plane", rings=8, az=4000)
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    prm = cil.make_params("point_to_plane", 20, 1.0, rot_tol=1e-5, trans_tol=1e-6)
+    res_t, log = cil.cil_icp_run(t, dev(w.target), dev(np.eye(4)), prm)
+    res = cil.decode_result(res_t)
+    assert res.converged and res.iterations == 1 and res.rmse == 0.0 and res.n_corr == w.n
+    assert (log.cpu().numpy()[1:] == 0).all()
+
+
+def test_deterministic(cil):
+    w = W.c4("point_to_plane", rings=16, az=8000)
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    prm = cil.make_params("point_to_plane", 10, 1.0)
+    a = cil.decode_result(cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)[0])
+    b = cil.decode_result(cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)[0])
+    assert np.array_equal(a.pose, b.pose) and a.rmse == b.rmse
+
+
+def test_icp_align_host_api(cil):
+    """the e2e public call from host arrays"""
+    w = W.c1()
+    res = cil.icp_align(w.target, w.target_normals, w.source, "point_to_plane", 20, 0.1)
+    o = oracle.icp_run(w.target, w.target_normals, w.source, "point_to_plane", 20, 0.1)
+    assert W.rot_angle(res.pose[:3, :3] @ o.pose[:3, :3].T) <= 1e-4
+    assert np.abs(res.pose[:3, 3] - o.pose[:3, 3]).max() <= 1e-5

@@ -4,13 +4,14 @@
 // on-device 6x6 Cholesky solve and pose update, so an iteration loop launches with no host
 // round-trip".
 //
-// One launch = one iteration:
-//   every thread, for its queries i = tid, tid + stride, ...:
-//     a1  s = R p_i + t (fp64) -> double-float
-//     a2  exact 1-NN over the BVH, bounded by max_corr_dist (warm-started in cil_icp_run by
-//         the previous iteration's match, which only tightens the initial bound)
-//     a3  reject: accepted iff a target with d^2 <= fl32(max_corr_dist^2) exists
-//     a4  residual + Jacobian of the metric (PAPER.md:140 [Besl], [Low])
+// One iteration = two launches:
+//   K_nn  (correspondence kernel, north_star subsystem (3)): persistent search engine
+//         (search.cuh) -- a1 s = R p_i + t (fp64 -> double-float), a2 exact 1-NN bounded by
+//         max_corr_dist (a3: nothing within the bound = rejected), hint leaf = the previous
+//         iteration's match in cil_icp_run; writes nn_pos[i] (sorted target position or -1).
+//   K_acc (fused transform+reject+J^TJ/J^Tr kernel, subsystem (4)), static grid-stride:
+//     a1  s = R p_i + t again (fp64 -> double-float)
+//     a4  residual + Jacobian of the metric for accepted pairs (PAPER.md:140 [Besl], [Low])
 //     a5  fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
 //   warp: transposed butterfly reduce (31 SHFL for 32 values; lane k ends with sum k)
 //   block: per-warp fp64 sums -> per-CTA fp64 partial in the workspace
@@ -41,7 +42,8 @@ struct IterArgs {
     cil_icp_system* sys;     // iterate only, nullable
     int32_t* corr_idx;       // iterate only, nullable
     float* corr_d2;          // iterate only, nullable
-    int* nn_prev;            // run only: warm-start match per query (sorted target position or -1)
+    int* nn_pos;             // [m] match per query (sorted target position or -1), written by K_nn
+    int warm;                // K_nn: use nn_pos as the hint (cil_icp_run after its first iteration)
     double* iter_log;        // run only, nullable
     int run;
     double rot_tol, trans_tol;
@@ -198,10 +200,53 @@ __device__ void finalize(const IterArgs& a, const double* S, const double* P) {
     }
 }
 
-// ---------------------------------------------------------------- the fused iteration
-template <int METRIC, int B>
+// ---------------------------------------------------------------- K_nn
+constexpr int kNNThreads = 256;
+
+template <int B>
+struct IcpQueries {
+    const float* src;
+    Pose34 P;
+    float bound2;
+    int* nn_pos;
+    int warm;
+    int32_t* corr_idx;
+    float* corr_d2;
+    __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
+        s = transform_df(P, src[3 * (size_t)i], src[3 * (size_t)i + 1], src[3 * (size_t)i + 2]);
+        init = bound_key(bound2);
+        const int jp = warm ? nn_pos[i] : -1;
+        hint = jp >= 0 ? jp / B : -1;
+        return true;
+    }
+    __device__ __forceinline__ void store(int i, unsigned long long best, int bpos, const DF3&) const {
+        const bool found = best != bound_key(bound2);
+        nn_pos[i] = found ? bpos : -1;
+        if (corr_idx) corr_idx[i] = found ? (int32_t)key_idx(best) : -1;
+        if (corr_d2) corr_d2[i] = found ? key_d2(best) : INFINITY;
+    }
+};
+
+template <int B>
+__global__ void __launch_bounds__(kNNThreads)
+icp_nn_kernel(const IterArgs a) {
+    if (a.run && *(volatile int*)&a.st->done) return;
+    IcpQueries<B> qs;
+    qs.src = a.src;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) qs.P.r[k] = __ldg(a.pose_in + k);
+    qs.bound2 = a.bound2;
+    qs.nn_pos = a.nn_pos;
+    qs.warm = a.warm;
+    qs.corr_idx = a.corr_idx;
+    qs.corr_d2 = a.corr_d2;
+    nn_packet_engine<B>(a.T, qs, a.m, &a.st->work);
+}
+
+// ---------------------------------------------------------------- K_acc (+ a6, a7)
+template <int METRIC>
 __global__ void __launch_bounds__(kIcpThreads)
-icp_iter_kernel(const IterArgs a) {
+icp_acc_kernel(const IterArgs a) {
     __shared__ double wsum[kIcpWarps][kSlots];
     __shared__ double Ssum[kSlots];
     __shared__ double Psh[16];
@@ -219,23 +264,12 @@ icp_iter_kernel(const IterArgs a) {
     for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
 
     const TargetView& T = a.T;
-    const unsigned long long none = bound_key(a.bound2);
     const int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += stride) {
-        const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
-        const DF3 s = transform_df(P, px, py, pz);                     // a1
-        unsigned long long best = none;
-        int bpos = -1;
-        if (a.nn_prev) {                                                // warm start: tighter bound
-            const int jp = a.nn_prev[i];
-            if (jp >= 0) offer(s, __ldg(T.pts + jp), jp, best, bpos);
-        }
-        bvh_nearest<B>(T, s, best, bpos);                               // a2
-        const bool acc_ok = best != none;                               // a3
-        if (a.nn_prev) a.nn_prev[i] = acc_ok ? bpos : -1;
-        if (a.corr_idx) a.corr_idx[i] = acc_ok ? (int32_t)key_idx(best) : -1;
-        if (a.corr_d2) a.corr_d2[i] = acc_ok ? key_d2(best) : INFINITY;
-        if (!acc_ok) continue;
+        const int bpos = a.nn_pos[i];
+        if (bpos < 0) continue;                                         // a3: rejected
+        const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1],
+                                   a.src[3 * (size_t)i + 2]);            // a1
         const float4 t = __ldg(T.pts + bpos);
         const float dx = dfdiff(s.hx, s.lx, t.x);
         const float dy = dfdiff(s.hy, s.ly, t.y);
@@ -304,6 +338,7 @@ icp_iter_kernel(const IterArgs a) {
     if (threadIdx.x == 0) {
         finalize<METRIC>(a, Ssum, Psh);
         a.st->ticket = 0;
+        a.st->work = 0;      // K_nn's counter, for the next iteration
     }
 }
 
@@ -314,7 +349,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn_p
     if (tid == 0) {
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
-        st->done = 0; st->ticket = 0;
+        st->done = 0; st->ticket = 0; st->work = 0;
     }
     for (int i = tid; i < m; i += gridDim.x * blockDim.x) nn_prev[i] = -1;
     if (iter_log)
@@ -332,36 +367,47 @@ __global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
     res->pad = 0;
 }
 
-__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; }
+__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; }
 
-template <int METRIC, int B>
-int icp_grid(int m) {
-    static int occ = -1;
-    if (occ < 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, icp_iter_kernel<METRIC, B>, kIcpThreads, 0) != cudaSuccess)
-            occ = 1;
-        occ = std::max(occ, 1);
-    }
-    int64_t want = ((int64_t)m + kIcpThreads - 1) / kIcpThreads;
-    int64_t cap = std::min<int64_t>((int64_t)sm_count() * occ, kMaxCtas);
+template <class K>
+int persistent_grid(K kernel, int threads, int m, int cap_ctas) {
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess) occ = 1;
+    occ = std::max(occ, 1);
+    const int64_t want = ((int64_t)m + threads - 1) / threads;
+    const int64_t cap = std::min<int64_t>((int64_t)sm_count() * occ, cap_ctas);
     return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
-template <int METRIC>
-cudaError_t launch_iter_m(const IterArgs& a, int B, cudaStream_t s) {
-    switch (B) {
-        case 4: icp_iter_kernel<METRIC, 4><<<icp_grid<METRIC, 4>(a.m), kIcpThreads, 0, s>>>(a); break;
-        case 8: icp_iter_kernel<METRIC, 8><<<icp_grid<METRIC, 8>(a.m), kIcpThreads, 0, s>>>(a); break;
-        case 16: icp_iter_kernel<METRIC, 16><<<icp_grid<METRIC, 16>(a.m), kIcpThreads, 0, s>>>(a); break;
-        default: icp_iter_kernel<METRIC, 32><<<icp_grid<METRIC, 32>(a.m), kIcpThreads, 0, s>>>(a); break;
-    }
+template <int B>
+cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
+    static int grid_cache[2] = {0, 0};
+    (void)grid_cache;
+    const int g = persistent_grid(icp_nn_kernel<B>, kNNThreads, a.m, 1 << 20);
+    icp_nn_kernel<B><<<g, kNNThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
+template <int METRIC>
+cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
+    const int g = persistent_grid(icp_acc_kernel<METRIC>, kIcpThreads, a.m, kMaxCtas);
+    icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// one ICP iteration = K_nn + K_acc
 cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
-    count_launches(1);
-    return metric == CIL_POINT_TO_PLANE ? launch_iter_m<CIL_POINT_TO_PLANE>(a, a.T.leaf_size, s)
-                                        : launch_iter_m<CIL_POINT_TO_POINT>(a, a.T.leaf_size, s);
+    count_launches(2);
+    cudaError_t e;
+    switch (a.T.leaf_size) {
+        case 4: e = launch_nn_b<4>(a, s); break;
+        case 8: e = launch_nn_b<8>(a, s); break;
+        case 16: e = launch_nn_b<16>(a, s); break;
+        default: e = launch_nn_b<32>(a, s); break;
+    }
+    if (e != cudaSuccess) return e;
+    return metric == CIL_POINT_TO_PLANE ? launch_acc_m<CIL_POINT_TO_PLANE>(a, s)
+                                        : launch_acc_m<CIL_POINT_TO_POINT>(a, s);
 }
 
 struct WsLayout {
@@ -436,7 +482,8 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     a.sys = sys;
     a.corr_idx = corr_idx;
     a.corr_d2 = corr_sqdist;
-    a.nn_prev = nullptr;
+    a.nn_pos = (int*)(w + L.nn_prev);
+    a.warm = 0;
     a.iter_log = nullptr;
     a.run = 0;
     cudaStream_t s = (cudaStream_t)stream;
@@ -465,18 +512,20 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.pose_in = a.st->pose;
     a.pose_out = a.st->pose;
     a.partials = (double*)(w + L.partials);
-    a.nn_prev = (int*)(w + L.nn_prev);
+    a.nn_pos = (int*)(w + L.nn_prev);
+    a.warm = 0;
     a.iter_log = iter_log;
     a.run = 1;
     a.rot_tol = params->rot_tol;
     a.trans_tol = params->trans_tol;
     cudaStream_t s = (cudaStream_t)stream;
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
-    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn_prev, (int)m, iter_log, 2 * params->max_iters);
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn_pos, (int)m, iter_log, 2 * params->max_iters);
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
     for (int it = 0; it < params->max_iters; ++it) {
+        a.warm = it > 0;
         e = launch_iter(a, params->metric, s);
         if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
     }

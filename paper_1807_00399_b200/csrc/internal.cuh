@@ -24,9 +24,15 @@ struct TargetView {
     const float4* pts;    // [n] sorted by Morton key: x, y, z, __int_as_float(original index)
     const float4* nrm;    // [n] normals in the same order (w unused) or nullptr
     const float4* box;    // [2 * 2 * l_pad]: node v (1-based heap) -> box[2v] = lo, box[2v+1] = hi
+    const float4* leafsoa;  // [n_leaves * B]: per leaf rows x[B], y[B], z[B], idx[B] (padding: +inf, idx ~0)
+    const unsigned long long* keys;  // [n] sorted 48-bit Morton keys of pts
+    const uint32_t* cell_first;      // [2^coarse_bits + 1]: first sorted index with key >> (48-coarse_bits) >= c
+    const float4* quant;  // [1]: (min.x, min.y, min.z, cells per unit) of the Morton quantisation
     int n;
     int l_pad;            // power of two >= number of leaves; leaves are nodes l_pad .. 2*l_pad-1
+    int levels;           // log2(l_pad)
     int leaf_size;
+    int coarse_bits;      // multiple of 3, <= 21
 };
 
 struct cil_target {
@@ -48,7 +54,8 @@ struct alignas(256) IcpState {
     int status;
     int done;
     unsigned int ticket;
-    int pad_[3];
+    unsigned int work;    // dynamic work counter of the correspondence kernel
+    int pad_[2];
 };
 
 namespace cil {

@@ -11,35 +11,42 @@ namespace {
 
 constexpr int kNNThreads = 256;
 
-template <int B>
-__global__ void __launch_bounds__(kNNThreads)
-nn_query_kernel(TargetView T, const float* __restrict__ q, int m, float bound2,
-                int32_t* __restrict__ idx, float* __restrict__ sqd) {
-    const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-        DF3 s;
+struct NNQueries {
+    const float* q;
+    float bound2;
+    int32_t* idx;
+    float* sqd;
+    __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
         s.hx = q[3 * (size_t)i]; s.hy = q[3 * (size_t)i + 1]; s.hz = q[3 * (size_t)i + 2];
         s.lx = s.ly = s.lz = 0.0f;
-        const unsigned long long none = bound_key(bound2);
-        unsigned long long best = none;
-        int bpos = -1;
-        bvh_nearest<B>(T, s, best, bpos);
-        const bool found = best != none;
+        init = bound_key(bound2);
+        hint = -1;
+        return true;
+    }
+    __device__ __forceinline__ void store(int i, unsigned long long best, int, const DF3&) const {
+        const bool found = best != bound_key(bound2);
         if (idx) idx[i] = found ? (int32_t)key_idx(best) : -1;
         if (sqd) sqd[i] = found ? key_d2(best) : INFINITY;
     }
+};
+
+template <int B>
+__global__ void __launch_bounds__(kNNThreads)
+nn_query_kernel(TargetView T, NNQueries qs, int m, unsigned int* counter) {
+    nn_packet_engine<B>(T, qs, m, counter);
 }
 
 template <int B>
-cudaError_t launch_nn(const TargetView& T, const float* q, int m, float bound2, int32_t* idx, float* sqd,
-                      cudaStream_t s) {
+cudaError_t launch_nn(const TargetView& T, const NNQueries& qs, int m, unsigned int* counter, cudaStream_t s) {
     static int occ = -1;   // per-process cache; all supported devices are sm_100a
     if (occ < 0) {
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nn_query_kernel<B>, kNNThreads, 0);
         if (e != cudaSuccess) return e;
+        occ = std::max(occ, 1);
     }
-    int blocks = (int)std::min<int64_t>(((int64_t)m + kNNThreads - 1) / kNNThreads, (int64_t)sm_count() * std::max(occ, 1));
-    nn_query_kernel<B><<<std::max(blocks, 1), kNNThreads, 0, s>>>(T, q, m, bound2, idx, sqd);
+    const int64_t want = ((int64_t)m + kNNThreads - 1) / kNNThreads;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
+    nn_query_kernel<B><<<blocks, kNNThreads, 0, s>>>(T, qs, m, counter);
     count_launches(1);
     return cudaGetLastError();
 }
@@ -57,15 +64,21 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     if (m == 0) return CIL_OK;
     if (!queries) { set_error("cil_nn_query: queries is NULL"); return CIL_ERR_INVALID_ARG; }
     if (!idx && !sqdist) return CIL_OK;
-    const float bound2 = std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist);
-    cudaError_t e;
+    NNQueries qs{queries, std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist),
+                 idx, sqdist};
     cudaStream_t s = (cudaStream_t)stream;
-    switch (t->v.leaf_size) {
-        case 4: e = launch_nn<4>(t->v, queries, (int)m, bound2, idx, sqdist, s); break;
-        case 8: e = launch_nn<8>(t->v, queries, (int)m, bound2, idx, sqdist, s); break;
-        case 16: e = launch_nn<16>(t->v, queries, (int)m, bound2, idx, sqdist, s); break;
-        default: e = launch_nn<32>(t->v, queries, (int)m, bound2, idx, sqdist, s); break;
+    unsigned int* counter = nullptr;   // dynamic work counter (stream-ordered scratch)
+    CIL_CUDA_TRY(cudaMallocAsync((void**)&counter, sizeof(unsigned int), s), "cudaMallocAsync(counter)");
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+    if (e == cudaSuccess) {
+        switch (t->v.leaf_size) {
+            case 4: e = launch_nn<4>(t->v, qs, (int)m, counter, s); break;
+            case 8: e = launch_nn<8>(t->v, qs, (int)m, counter, s); break;
+            case 16: e = launch_nn<16>(t->v, qs, (int)m, counter, s); break;
+            default: e = launch_nn<32>(t->v, qs, (int)m, counter, s); break;
+        }
     }
+    cudaFreeAsync(counter, s);
     if (e != cudaSuccess) return cuda_fail(e, "nn_query_kernel launch");
     return CIL_OK;
 }

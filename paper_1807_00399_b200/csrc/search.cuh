@@ -1,14 +1,30 @@
 // search.cuh -- device side of the exact 1-NN search.
 //
+// Index: target points sorted by 48-bit Morton key, grouped into leaves of B consecutive
+// points, with an implicit complete binary tree of AABBs over the leaves (node v has
+// children 2v, 2v+1; leaves are nodes l_pad .. 2 l_pad - 1).
+//
+// Search ("hint leaf, then ascend"): evaluate a hint leaf (the warm-start match of the
+// previous ICP iteration, or the leaf holding the first target of the query's coarse Morton
+// cell), then walk up the ancestors of that leaf.  At each ancestor u:
+//   * STOP if the ball B(s, sqrt(best)) provably holds no target outside u's subtree:
+//     every target in the ball has a Morton key in [code(ball_lo), code(ball_hi)] (the key is
+//     monotone in each quantised coordinate; one quantum of margin absorbs rounding), and
+//     u's subtree is exactly the sorted key range [key[a], key[b-1]]; so if
+//     key[a-1] < code(ball_lo) and code(ball_hi) < key[b] nothing outside can be in the ball;
+//   * otherwise test u's sibling box and search it (nearest-child-first DFS) if its lower
+//     bound does not exceed the best distance.
+// The subtrees of the siblings of all ancestors partition the tree, so the search is exact.
+//
 // Precision contract:
 //  * the transformed query s = R p + t is computed in fp64 and carried as a double-float
 //    pair (hi = fl32(s), lo = fl32(s - hi)), never materialised in fp32 alone;
-//  * per candidate the difference is (s_hi - t) + s_lo in fp32 -- exact-ish to ~1 ulp of
+//  * per candidate the difference is (s_hi - t) + s_lo in fp32 -- accurate to ~1 ulp of
 //    |s - t| rather than of |s| -- and d^2 = fma(dx,dx, fma(dy,dy, dz*dz)) in fp32;
 //  * the minimum is taken over the u64 key (bits(d^2) << 32) | original_index, which orders
 //    by d^2 (non-negative IEEE floats order like their bit patterns) and breaks exact ties
 //    by the lowest original index (R1);
-//  * a BVH node is pruned iff its lower bound lb^2 > best d^2, where lb is computed with the
+//  * a box is pruned iff its lower bound lb^2 > best d^2, where lb is computed with the
 //    SAME rounded operations as the candidate differences, so by monotonicity of IEEE
 //    rounding lb^2 <= d^2 of every point inside the box: pruning never drops a point that
 //    could win (or tie) under the kernel's own arithmetic -- the search is exact.
@@ -49,6 +65,30 @@ __device__ __forceinline__ DF3 transform_df(const Pose34& P, float px, float py,
     return split_df(x, y, z);
 }
 
+// ---------------------------------------------------------------- Morton quantisation
+// (used identically by the index build and by the search's containment test)
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {
+    x &= 0xffffull;                                  // 16 bits -> every third bit of 48
+    x = (x | (x << 16)) & 0x0000ff0000ffull;
+    x = (x | (x << 8)) & 0x00f00f00f00full;
+    x = (x | (x << 4)) & 0x0c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x249249249249ull;
+    return x;
+}
+
+__device__ __forceinline__ unsigned quantize1(float x, float mn, float sc) {
+    return (unsigned)fminf(fmaxf((x - mn) * sc, 0.0f), (float)((1 << kMortonBits) - 1));
+}
+
+__device__ __forceinline__ unsigned long long morton3(unsigned qx, unsigned qy, unsigned qz) {
+    return (spread3(qx) << 2) | (spread3(qy) << 1) | spread3(qz);
+}
+
+__device__ __forceinline__ unsigned long long morton_of(float4 Q, float x, float y, float z) {
+    return morton3(quantize1(x, Q.x, Q.w), quantize1(y, Q.y, Q.w), quantize1(z, Q.z, Q.w));
+}
+
+// ---------------------------------------------------------------- keys and distances
 __device__ __forceinline__ unsigned long long make_key(float d2, uint32_t idx) {
     return ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned long long)idx;
 }
@@ -77,60 +117,278 @@ __device__ __forceinline__ float box_lb2(const DF3& s, float4 lo, float4 hi) {
     return fmaf(gx, gx, fmaf(gy, gy, gz * gz));
 }
 
+__device__ __forceinline__ float node_lb2(const TargetView& T, const DF3& s, int v) {
+    const float4* bx = T.box + 2 * (size_t)v;
+    return box_lb2(s, __ldg(bx), __ldg(bx + 1));
+}
+
 // Evaluate candidate at sorted position j; keep the best key and its sorted position.
 __device__ __forceinline__ void offer(const DF3& s, float4 t, int j, unsigned long long& best, int& bpos) {
     unsigned long long k = make_key(cand_d2(s, t), (uint32_t)__float_as_int(t.w));
     if (k < best) { best = k; bpos = j; }
 }
 
+// ---------------------------------------------------------------- leaf evaluation
+// A leaf is a block of B consecutive sorted targets stored as rows x[B], y[B], z[B], idx[B]
+// (leafsoa).  Two candidates per instruction with the sm_100 packed FP32 ops (FADD2, FFMA2,
+// FMUL2): -dx = (t + (-s_hi)) + (-s_lo) is exactly the negation of (s_hi - t) + s_lo (IEEE
+// rounding is sign-symmetric), so d^2 is bit-identical to cand_d2().
+struct NegQuery {
+    float2 hx, hy, hz, lx, ly, lz;   // broadcast -s_hi, -s_lo
+};
+
+__device__ __forceinline__ NegQuery neg_query(const DF3& s) {
+    NegQuery q;
+    q.hx = make_float2(-s.hx, -s.hx); q.hy = make_float2(-s.hy, -s.hy); q.hz = make_float2(-s.hz, -s.hz);
+    q.lx = make_float2(-s.lx, -s.lx); q.ly = make_float2(-s.ly, -s.ly); q.lz = make_float2(-s.lz, -s.lz);
+    return q;
+}
+
+__device__ __forceinline__ float2 pair_d2(const NegQuery& q, float2 x, float2 y, float2 z) {
+    const float2 dx = __fadd2_rn(__fadd2_rn(x, q.hx), q.lx);
+    const float2 dy = __fadd2_rn(__fadd2_rn(y, q.hy), q.ly);
+    const float2 dz = __fadd2_rn(__fadd2_rn(z, q.hz), q.lz);
+    return __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+}
+
+template <int B>
+__device__ __forceinline__ void eval_leaf(const TargetView& T, const NegQuery& q, int leaf,
+                                          unsigned long long& best, int& bpos) {
+    constexpr int R = B / 4;                                   // float4 per row
+    const float4* blk = T.leafsoa + (size_t)leaf * (4 * R);
+    float d2[B];
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+        const float4 X = __ldg(blk + c), Y = __ldg(blk + R + c), Z = __ldg(blk + 2 * R + c);
+        const float2 a = pair_d2(q, make_float2(X.x, X.y), make_float2(Y.x, Y.y), make_float2(Z.x, Z.y));
+        const float2 b = pair_d2(q, make_float2(X.z, X.w), make_float2(Y.z, Y.w), make_float2(Z.z, Z.w));
+        d2[4 * c + 0] = a.x; d2[4 * c + 1] = a.y; d2[4 * c + 2] = b.x; d2[4 * c + 3] = b.y;
+    }
+    float mn = d2[0];
+#pragma unroll
+    for (int c = 1; c < B; ++c) mn = fminf(mn, d2[c]);
+    if (mn <= key_d2(best)) {                                   // an improvement or a tie is possible
+        const int* ids = reinterpret_cast<const int*>(blk + 3 * R);
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+            if (d2[c] == mn) {
+                const unsigned long long k = make_key(mn, (uint32_t)__ldg(ids + c));
+                if (k < best) { best = k; bpos = leaf * B + c; }
+            }
+        }
+    }
+}
+
+// Morton codes bounding every target that may lie in the ball B(s, sqrt(r2)).
+__device__ __forceinline__ void ball_codes(const float4 Q, const DF3& s, float r2,
+                                           unsigned long long& clo, unsigned long long& chi) {
+    const unsigned qmax = (1u << kMortonBits) - 1u;
+    if (!(r2 < INFINITY)) { clo = 0ull; chi = ~0ull; return; }
+    const float r = sqrtf(r2) * 1.000001f + 1e-30f;
+    unsigned lx = quantize1((s.hx - r) + s.lx, Q.x, Q.w), hx = quantize1((s.hx + r) + s.lx, Q.x, Q.w);
+    unsigned ly = quantize1((s.hy - r) + s.ly, Q.y, Q.w), hy = quantize1((s.hy + r) + s.ly, Q.y, Q.w);
+    unsigned lz = quantize1((s.hz - r) + s.lz, Q.z, Q.w), hz = quantize1((s.hz + r) + s.lz, Q.z, Q.w);
+    // one quantum of margin against rounding in the quantisation of the ball corners
+    lx = lx > 0 ? lx - 1 : 0; ly = ly > 0 ? ly - 1 : 0; lz = lz > 0 ? lz - 1 : 0;
+    hx = hx < qmax ? hx + 1 : qmax; hy = hy < qmax ? hy + 1 : qmax; hz = hz < qmax ? hz + 1 : qmax;
+    clo = morton3(lx, ly, lz);
+    chi = morton3(hx, hy, hz);
+}
+
+// Leaf whose first point is the first target of the query's coarse Morton cell (or the next
+// non-empty cell): a cold-start hint.
+__device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& s) {
+    const float4 Q = __ldg(T.quant);
+    const unsigned long long code = morton_of(Q, s.hx, s.hy, s.hz);
+    const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
+    int pos = (int)__ldg(T.cell_first + c);
+    pos = min(pos, T.n - 1);
+    return pos / T.leaf_size;
+}
+
+// ---------------------------------------------------------------- per-lane search state
+struct NoStats {
+    __device__ __forceinline__ void node() {}
+    __device__ __forceinline__ void leaf() {}
+    __device__ __forceinline__ void level() {}
+};
+struct CountStats {
+    int nodes = 0, leaves = 0, levels = 0;
+    __device__ __forceinline__ void node() { ++nodes; }
+    __device__ __forceinline__ void leaf() { ++leaves; }
+    __device__ __forceinline__ void level() { ++levels; }
+};
+
 constexpr int kMaxDepth = 32;
 
-// Exact nearest neighbour of s over the implicit BVH: nearest-child-first depth-first
-// traversal with a short stack; `best`/`bpos` carry in an initial bound (bound_key or a
-// warm-start candidate) and carry out the result.
-template <int B>
-__device__ __forceinline__ void bvh_nearest(const TargetView& T, const DF3& s,
-                                            unsigned long long& best, int& bpos) {
-    int stk_v[kMaxDepth];
-    float stk_lb[kMaxDepth];
-    int sp = 0;
-    int v = 1;
+struct LaneSearch {
+    DF3 s;
+    unsigned long long best;
+    int bpos;
+    int sp;            // DFS stack depth
+    int k;             // ascent level (0 = the hint leaf itself)
+    int u;             // current ancestor node
+    float r2;          // radius^2 the ball codes were computed for
+    unsigned long long clo, chi;
+};
+
+// DFS stack of one lane (local memory, kept apart from the register-resident LaneSearch)
+struct LaneStack {
+    int v[kMaxDepth];
+    float lb[kMaxDepth];
+};
+
+__device__ __forceinline__ void lane_start(LaneSearch& L, const TargetView& T, const DF3& s,
+                                           unsigned long long init, int hint_leaf) {
+    L.s = s;
+    L.best = init;
+    L.bpos = -1;
+    L.sp = 0;
+    L.k = 0;
+    L.u = T.l_pad + hint_leaf;
+    L.r2 = -1.0f;
+}
+
+// Advance this lane's search to the next leaf that must be evaluated; returns the leaf or -1
+// when the search is complete (see the header comment for the ascent / containment rule).
+template <class Stats>
+__device__ __forceinline__ int next_leaf(LaneSearch& L, LaneStack& K, const TargetView& T, Stats* st) {
+    while (true) {
+        if (L.sp > 0) {
+            --L.sp;
+            int v = K.v[L.sp];
+            if (K.lb[L.sp] > key_d2(L.best)) continue;
+            while (v < T.l_pad) {
+                if (st) st->node();
+                const int c = 2 * v;
+                const float4* bx = T.box + 2 * (size_t)c;
+                const float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
+                const float lb0 = box_lb2(L.s, lo0, hi0);
+                const float lb1 = box_lb2(L.s, lo1, hi1);
+                const float bd = key_d2(L.best);
+                const bool g0 = lb0 <= bd, g1 = lb1 <= bd;
+                if (g0 && g1) {
+                    const bool right_first = lb1 < lb0;
+                    K.v[L.sp] = right_first ? c : c + 1;
+                    K.lb[L.sp] = right_first ? lb0 : lb1;
+                    ++L.sp;
+                    v = right_first ? c + 1 : c;
+                } else if (g0) {
+                    v = c;
+                } else if (g1) {
+                    v = c + 1;
+                } else {
+                    v = -1;
+                    break;
+                }
+            }
+            if (v >= 0) return v - T.l_pad;
+            continue;
+        }
+        if (L.k >= T.levels) return -1;
+        if (st) st->level();
+        const float bd = key_d2(L.best);
+        if (bd != L.r2) { ball_codes(__ldg(T.quant), L.s, bd, L.clo, L.chi); L.r2 = bd; }
+        const int a = min(((L.u << L.k) - T.l_pad) * T.leaf_size, T.n);
+        const int b = min((((L.u + 1) << L.k) - T.l_pad) * T.leaf_size, T.n);
+        const bool lo_in = a == 0 || __ldg(T.keys + a - 1) < L.clo;
+        const bool hi_in = b >= T.n || L.chi < __ldg(T.keys + b);
+        if (lo_in && hi_in) { L.k = T.levels; return -1; }
+        const int sib = L.u ^ 1;
+        const float lb = node_lb2(T, L.s, sib);
+        ++L.k;
+        L.u >>= 1;
+        if (lb <= bd) {
+            K.v[0] = sib;
+            K.lb[0] = lb;
+            L.sp = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- warp-packet engine
+// A warp takes 32 consecutive queries (one per lane; consecutive = spatially coherent for
+// Morton- or scan-ordered inputs).  Phase 1: every lane evaluates its own hint leaf (its
+// warm-start match, or the coarse-cell hint), which gives each lane a tight bound.  Phase 2:
+// the warp walks the BVH together, top-down and nearest-first: a node is entered iff its box
+// lower bound is <= the best distance of at least one lane (ballot), so every lane sees every
+// node its own ball touches -- each lane's result is its exact nearest neighbour.  Box loads
+// are warp-uniform (broadcast), leaves are evaluated by all lanes with packed FP32, and the
+// DFS stack is held one entry per lane in a register, so control flow never diverges.
+// Q supplies
+//   __device__ bool load(int i, DF3& s, unsigned long long& init, int& hint_leaf)
+//   __device__ void store(int i, unsigned long long best, int bpos, const DF3& s)
+template <int B, class Q, class Stats = NoStats>
+__device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int m, unsigned int* counter,
+                                                 Stats* st = nullptr) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
     const int l_pad = T.l_pad;
     while (true) {
-        if (v >= l_pad) {
-            const int beg = (v - l_pad) * B;
-            const int cnt = min(B, T.n - beg);
-            float4 t[B];
-#pragma unroll
-            for (int q = 0; q < B; ++q)
-                if (q < cnt) t[q] = __ldg(T.pts + beg + q);
-#pragma unroll
-            for (int q = 0; q < B; ++q)
-                if (q < cnt) offer(s, t[q], beg + q, best, bpos);
-        } else {
-            const int c = 2 * v;
-            const float4* bx = T.box + 2 * c;
-            float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
-            float lb0 = box_lb2(s, lo0, hi0);
-            float lb1 = box_lb2(s, lo1, hi1);
-            const float bd = key_d2(best);
-            const bool g0 = lb0 <= bd, g1 = lb1 <= bd;
-            if (g0 && g1) {
-                const bool right_first = lb1 < lb0;
-                stk_v[sp] = right_first ? c : c + 1;
-                stk_lb[sp] = right_first ? lb0 : lb1;
-                ++sp;
-                v = right_first ? c + 1 : c;
-                continue;
-            }
-            if (g0) { v = c; continue; }
-            if (g1) { v = c + 1; continue; }
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd(counter, 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= m) break;
+        const int qi = base + lane;
+        DF3 s;
+        unsigned long long best = 0ull;
+        int bpos = -1;
+        int hint = -1;
+        bool active = false;
+        if (qi < m) {
+            active = qs.load(qi, s, best, hint);
+            if (active && hint < 0) hint = coarse_hint_leaf(T, s);
         }
-        const float bd = key_d2(best);
-        while (sp > 0 && stk_lb[sp - 1] > bd) --sp;
-        if (sp == 0) break;
-        --sp;
-        v = stk_v[sp];
+        if (!active) {            // inactive lanes: a point far away that never asks for a node
+            s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f;
+            best = make_key(-1.0f, 0u);   // negative radius: every lower bound exceeds it
+        }
+        const NegQuery nq = neg_query(s);
+        if (active) {
+            if (st) st->leaf();
+            eval_leaf<B>(T, nq, hint, best, bpos);
+        }
+        // phase 2: converged top-down traversal
+        int stk = 0;              // lane k holds stack entry k
+        int sp = 0;               // warp-uniform stack depth
+        int v = 1;
+        while (true) {
+            if (v >= l_pad) {
+                if (st) st->leaf();
+                eval_leaf<B>(T, nq, v - l_pad, best, bpos);
+            } else {
+                if (st) st->node();
+                const int c = 2 * v;
+                const float4* bx = T.box + 2 * (size_t)c;
+                const float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
+                const float bd = key_d2(best);
+                const float lb0 = box_lb2(s, lo0, hi0), lb1 = box_lb2(s, lo1, hi1);
+                const unsigned m0 = __ballot_sync(FULL, lb0 <= bd);
+                const unsigned m1 = __ballot_sync(FULL, lb1 <= bd);
+                if (m0 && m1) {
+                    // nearer child first: the one more lanes prefer
+                    const unsigned pref1 = __ballot_sync(FULL, lb1 < lb0);
+                    const bool right_first = __popc(pref1 & (m0 | m1)) * 2 > __popc(m0 | m1);
+                    const int far_ = right_first ? c : c + 1;
+                    if (lane == sp) stk = far_;
+                    ++sp;
+                    v = right_first ? c + 1 : c;
+                    continue;
+                }
+                if (m0) { v = c; continue; }
+                if (m1) { v = c + 1; continue; }
+            }
+            // pop, skipping subtrees no lane needs any more
+            bool found = false;
+            while (sp > 0) {
+                --sp;
+                const int cand = __shfl_sync(FULL, stk, sp);
+                const float lb = node_lb2(T, s, cand);
+                if (__any_sync(FULL, lb <= key_d2(best))) { v = cand; found = true; break; }
+            }
+            if (!found) break;
+        }
+        if (active) qs.store(qi, best, bpos, s);
     }
 }
 

@@ -10,6 +10,7 @@
 //   K5  leaf AABBs (leaf_size consecutive sorted points), then internal AABBs level by level
 //       of an implicit complete binary tree (node v has children 2v, 2v+1).
 #include "internal.cuh"
+#include "search.cuh"
 
 #include <algorithm>
 #include <cfloat>
@@ -54,8 +55,8 @@ __global__ void bbox_partial_kernel(const float* __restrict__ p, int n, float* _
     }
 }
 
-// bbox[0..2] = min, bbox[3] = scale (cells per unit), bbox[4..5] unused
-__global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, float* __restrict__ bbox) {
+// quant = (min.x, min.y, min.z, cells per unit)
+__global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, float4* __restrict__ quant) {
     if (threadIdx.x != 0) return;
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (int b = 0; b < nblk; ++b)
@@ -65,30 +66,14 @@ __global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, floa
         }
     float ext = fmaxf(fmaxf(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
     float cells = (float)((1 << kMortonBits) - 1);
-    bbox[0] = mn[0]; bbox[1] = mn[1]; bbox[2] = mn[2];
-    bbox[3] = ext > 0.0f ? cells / ext : 0.0f;
+    *quant = make_float4(mn[0], mn[1], mn[2], ext > 0.0f ? cells / ext : 0.0f);
 }
 
-__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {
-    // 16 bits -> every third bit of a 48-bit word
-    x &= 0xffffull;
-    x = (x | (x << 16)) & 0x0000ff0000ffull;
-    x = (x | (x << 8)) & 0x00f00f00f00full;
-    x = (x | (x << 4)) & 0x0c30c30c30c3ull;
-    x = (x | (x << 2)) & 0x249249249249ull;
-    return x;
-}
-
-__global__ void morton_kernel(const float* __restrict__ p, int n, const float* __restrict__ bbox,
+__global__ void morton_kernel(const float* __restrict__ p, int n, const float4* __restrict__ quant,
                               unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
-    const float mx = bbox[0], my = bbox[1], mz = bbox[2], sc = bbox[3];
-    const float cmax = (float)((1 << kMortonBits) - 1);
+    const float4 Q = *quant;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        float x = p[3 * (size_t)i], y = p[3 * (size_t)i + 1], z = p[3 * (size_t)i + 2];
-        unsigned qx = (unsigned)fminf(fmaxf((x - mx) * sc, 0.0f), cmax);
-        unsigned qy = (unsigned)fminf(fmaxf((y - my) * sc, 0.0f), cmax);
-        unsigned qz = (unsigned)fminf(fmaxf((z - mz) * sc, 0.0f), cmax);
-        keys[i] = (spread3(qx) << 2) | (spread3(qy) << 1) | spread3(qz);
+        keys[i] = morton_of(Q, p[3 * (size_t)i], p[3 * (size_t)i + 1], p[3 * (size_t)i + 2]);
         vals[i] = (uint32_t)i;
     }
 }
@@ -215,6 +200,21 @@ __global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, in
     }
 }
 
+// SoA leaf blocks: leaf L holds rows x[B], y[B], z[B], idx[B]; padding slots get +inf / ~0
+__global__ void leaf_soa_kernel(const float4* __restrict__ pts, int n, int B, int64_t n_leaves, float* __restrict__ soa) {
+    const int64_t total = n_leaves * B;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t leaf = g / B;
+        const int q = (int)(g % B);
+        float4 t = g < n ? pts[g] : make_float4(INFINITY, INFINITY, INFINITY, __int_as_float(-1));
+        float* blk = soa + leaf * 4 * B;
+        blk[q] = t.x;
+        blk[B + q] = t.y;
+        blk[2 * B + q] = t.z;
+        blk[3 * B + q] = t.w;
+    }
+}
+
 // nodes [first, 2*first) from their children
 __global__ void level_box_kernel(float4* __restrict__ box, int first) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < first; k += gridDim.x * blockDim.x) {
@@ -222,6 +222,18 @@ __global__ void level_box_kernel(float4* __restrict__ box, int first) {
         float4 l0 = box[2 * c], h0 = box[2 * c + 1], l1 = box[2 * c + 2], h1 = box[2 * c + 3];
         box[2 * v] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.0f);
         box[2 * v + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.0f);
+    }
+}
+
+// cell_first[c] = first sorted index whose key >> shift >= c, for c in [0, ncell]
+__global__ void cell_first_kernel(const unsigned long long* __restrict__ keys, int n, int shift, uint32_t ncell,
+                                  uint32_t* __restrict__ cell_first) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long c = (long long)(keys[i] >> shift);
+        const long long cp = i > 0 ? (long long)(keys[i - 1] >> shift) : -1;
+        for (long long q = cp + 1; q <= c; ++q) cell_first[q] = (uint32_t)i;
+        if (i == n - 1)
+            for (long long q = c + 1; q <= (long long)ncell; ++q) cell_first[q] = (uint32_t)n;
     }
 }
 
@@ -259,11 +271,22 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     int64_t l_pad = 1;
     while (l_pad < n_leaves) l_pad <<= 1;
 
-    // one allocation: pts (16N), nrm (16N), box (2 * 2*l_pad * 16)
+    int levels = 0;
+    while ((1ll << levels) < l_pad) ++levels;
+    // coarse Morton cells: about one cell per point, a multiple of 3 bits, at most 21
+    int coarse_bits = 3;
+    while (coarse_bits < 21 && (1ll << coarse_bits) < n) coarse_bits += 3;
+    const int64_t ncell = 1ll << coarse_bits;
+
+    // one allocation: pts (16N), nrm (16N), box (2 * 2*l_pad * 16), keys (8N), cell table, quant
     const size_t b_pts = align_up((size_t)N * 16, 256);
     const size_t b_nrm = normals ? align_up((size_t)N * 16, 256) : 0;
     const size_t b_box = align_up((size_t)4 * l_pad * 16, 256);
-    const size_t bytes = b_pts + b_nrm + b_box;
+    const size_t b_keys = align_up((size_t)N * 8, 256);
+    const size_t b_cell = align_up((size_t)(ncell + 1) * 4, 256);
+    const size_t b_quant = 256;
+    const size_t b_soa = align_up((size_t)n_leaves * B * 16, 256);
+    const size_t bytes = b_pts + b_nrm + b_box + b_keys + b_cell + b_quant + b_soa;
     int dev = 0;
     CIL_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
     void* mem = nullptr;
@@ -272,13 +295,17 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     float4* d_pts = (float4*)base;
     float4* d_nrm = normals ? (float4*)(base + b_pts) : nullptr;
     float4* d_box = (float4*)(base + b_pts + b_nrm);
+    unsigned long long* d_keys = (unsigned long long*)(base + b_pts + b_nrm + b_box);
+    uint32_t* d_cell = (uint32_t*)(base + b_pts + b_nrm + b_box + b_keys);
+    float4* d_quant = (float4*)(base + b_pts + b_nrm + b_box + b_keys + b_cell);
+    float* d_soa = (float*)(base + b_pts + b_nrm + b_box + b_keys + b_cell + b_quant);
 
     // scratch: keys x2 (8N), vals x2 (4N), hist (256 * nblk), bbox partials
     const int nblk_sort = (N + kTile - 1) / kTile;
     const int nblk_bbox = grid_for(N);
     const size_t s_keys = align_up((size_t)N * 8, 256), s_vals = align_up((size_t)N * 4, 256);
     const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
-    const size_t s_bb = align_up((size_t)(6 * nblk_bbox + 8) * 4, 256);
+    const size_t s_bb = align_up((size_t)(6 * nblk_bbox) * 4, 256);
     const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb;
     void* tmp = nullptr;
     cudaError_t e = cudaMallocAsync(&tmp, scratch, s);
@@ -290,11 +317,10 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     uint32_t* v1 = (uint32_t*)(tb + 2 * s_keys + s_vals);
     uint32_t* hist = (uint32_t*)(tb + 2 * s_keys + 2 * s_vals);
     float* bbp = (float*)(tb + 2 * s_keys + 2 * s_vals + s_hist);
-    float* bbox = bbp + 6 * nblk_bbox;
 
     bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, N, bbp);
-    bbox_final_kernel<<<1, 32, 0, s>>>(bbp, nblk_bbox, bbox);
-    morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, bbox, k0, v0);
+    bbox_final_kernel<<<1, 32, 0, s>>>(bbp, nblk_bbox, d_quant);
+    morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, d_quant, k0, v0);
     for (int shift = 0; shift < 3 * kMortonBits; shift += kRadixBits) {
         radix_hist_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, N, shift, hist, nblk_sort);
         scan_kernel<<<1, 1024, 0, s>>>(hist, kRadix * nblk_sort);
@@ -303,13 +329,16 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
         std::swap(v0, v1);
     }
     gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, d_pts, d_nrm);
+    cudaMemcpyAsync(d_keys, k0, (size_t)N * 8, cudaMemcpyDeviceToDevice, s);
+    cell_first_kernel<<<grid_for(N), kThreads, 0, s>>>(k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
     leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(d_pts, N, B, (int)l_pad, d_box);
+    leaf_soa_kernel<<<grid_for(n_leaves * B), kThreads, 0, s>>>(d_pts, N, B, n_leaves, d_soa);
     for (int64_t first = l_pad / 2; first >= 1; first /= 2)
         level_box_kernel<<<grid_for(first), kThreads, 0, s>>>(d_box, (int)first);
     {
         int levels = 0;
         for (int64_t f = l_pad / 2; f >= 1; f /= 2) ++levels;
-        count_launches(3 + 3 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + 2 + levels);
+        count_launches(3 + 3 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + 4 + levels);
     }
     e = cudaGetLastError();
     cudaFreeAsync(tmp, s);
@@ -322,6 +351,12 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     t->v.n = N;
     t->v.l_pad = (int)l_pad;
     t->v.leaf_size = B;
+    t->v.keys = d_keys;
+    t->v.leafsoa = (const float4*)d_soa;
+    t->v.cell_first = d_cell;
+    t->v.quant = d_quant;
+    t->v.levels = levels;
+    t->v.coarse_bits = coarse_bits;
     t->n_leaves = n_leaves;
     t->has_normals = normals ? 1 : 0;
     t->device = dev;

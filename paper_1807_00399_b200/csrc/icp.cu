@@ -370,10 +370,13 @@ __global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
 __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; }
 
 template <class K>
-int persistent_grid(K kernel, int threads, int m, int cap_ctas) {
+int occupancy_of(K kernel, int threads) {
     int occ = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess) occ = 1;
-    occ = std::max(occ, 1);
+    return std::max(occ, 1);
+}
+
+inline int persistent_grid(int occ, int threads, int m, int cap_ctas) {
     const int64_t want = ((int64_t)m + threads - 1) / threads;
     const int64_t cap = std::min<int64_t>((int64_t)sm_count() * occ, cap_ctas);
     return (int)std::max<int64_t>(1, std::min(want, cap));
@@ -381,16 +384,16 @@ int persistent_grid(K kernel, int threads, int m, int cap_ctas) {
 
 template <int B>
 cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
-    static int grid_cache[2] = {0, 0};
-    (void)grid_cache;
-    const int g = persistent_grid(icp_nn_kernel<B>, kNNThreads, a.m, 1 << 20);
+    static const int occ = occupancy_of(icp_nn_kernel<B>, kNNThreads);
+    const int g = persistent_grid(occ, kNNThreads, a.m, 1 << 20);
     icp_nn_kernel<B><<<g, kNNThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int METRIC>
 cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
-    const int g = persistent_grid(icp_acc_kernel<METRIC>, kIcpThreads, a.m, kMaxCtas);
+    static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads);
+    const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
     icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -70,6 +70,10 @@ void count_launches(int k);   // diagnostics counter behind cil_launch_count()
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
+size_t scan_temp_bytes(int64_t len);
+int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s);
+
 }  // namespace cil
 
 #define CIL_CUDA_TRY(expr, what)                              \

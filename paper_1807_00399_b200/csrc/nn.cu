@@ -11,24 +11,48 @@ namespace {
 
 constexpr int kNNThreads = 256;
 
+// Queries are processed in the order of perm (a counting sort by the target's coarse Morton
+// cell) so that the 32 queries of a warp packet are spatial neighbours; results are written
+// back in the caller's order.
 struct NNQueries {
     const float* q;
+    const uint32_t* perm;
     float bound2;
     int32_t* idx;
     float* sqd;
-    __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
-        s.hx = q[3 * (size_t)i]; s.hy = q[3 * (size_t)i + 1]; s.hz = q[3 * (size_t)i + 2];
+    __device__ __forceinline__ bool load(int k, DF3& s, unsigned long long& init, int& hint) const {
+        const size_t i = perm[k];
+        s.hx = q[3 * i]; s.hy = q[3 * i + 1]; s.hz = q[3 * i + 2];
         s.lx = s.ly = s.lz = 0.0f;
         init = bound_key(bound2);
         hint = -1;
         return true;
     }
-    __device__ __forceinline__ void store(int i, unsigned long long best, int, const DF3&) const {
+    __device__ __forceinline__ void store(int k, unsigned long long best, int, const DF3&) const {
+        const size_t i = perm[k];
         const bool found = best != bound_key(bound2);
         if (idx) idx[i] = found ? (int32_t)key_idx(best) : -1;
         if (sqd) sqd[i] = found ? key_d2(best) : INFINITY;
     }
 };
+
+// counting sort of the queries by coarse cell: count, (scan), scatter
+__global__ void qcell_count_kernel(TargetView T, const float* __restrict__ q, int m, uint32_t* __restrict__ qcell,
+                                   uint32_t* __restrict__ cnt) {
+    const float4 Q = __ldg(T.quant);
+    const int shift = 3 * kMortonBits - T.coarse_bits;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const uint32_t c = (uint32_t)(morton_of(Q, q[3 * (size_t)i], q[3 * (size_t)i + 1], q[3 * (size_t)i + 2]) >> shift);
+        qcell[i] = c;
+        atomicAdd(cnt + c, 1u);
+    }
+}
+
+__global__ void qcell_scatter_kernel(const uint32_t* __restrict__ qcell, int m, uint32_t* __restrict__ cursor,
+                                     uint32_t* __restrict__ perm) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        perm[atomicAdd(cursor + qcell[i], 1u)] = (uint32_t)i;
+}
 
 template <int B>
 __global__ void __launch_bounds__(kNNThreads)
@@ -64,13 +88,29 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     if (m == 0) return CIL_OK;
     if (!queries) { set_error("cil_nn_query: queries is NULL"); return CIL_ERR_INVALID_ARG; }
     if (!idx && !sqdist) return CIL_OK;
-    NNQueries qs{queries, std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist),
-                 idx, sqdist};
     cudaStream_t s = (cudaStream_t)stream;
-    unsigned int* counter = nullptr;   // dynamic work counter (stream-ordered scratch)
-    CIL_CUDA_TRY(cudaMallocAsync((void**)&counter, sizeof(unsigned int), s), "cudaMallocAsync(counter)");
-    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+    // stream-ordered scratch: work counter | cell counts | qcell | perm | scan temp
+    const int64_t ncell = 1ll << t->v.coarse_bits;
+    const size_t b_cnt = align_up((size_t)(ncell + 1) * 4, 256);
+    const size_t b_q = align_up((size_t)m * 4, 256);
+    const size_t b_scan = scan_temp_bytes(ncell + 1);
+    void* scratch = nullptr;
+    CIL_CUDA_TRY(cudaMallocAsync(&scratch, 256 + b_cnt + 2 * b_q + b_scan, s), "cudaMallocAsync(nn scratch)");
+    char* sb = (char*)scratch;
+    unsigned int* counter = (unsigned int*)sb;
+    uint32_t* cnt = (uint32_t*)(sb + 256);
+    uint32_t* qcell = (uint32_t*)(sb + 256 + b_cnt);
+    uint32_t* perm = (uint32_t*)(sb + 256 + b_cnt + b_q);
+    void* scan_tmp = (void*)(sb + 256 + b_cnt + 2 * b_q);
+    cudaError_t e = cudaMemsetAsync(sb, 0, 256 + b_cnt, s);
+    NNQueries qs{queries, perm, std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist),
+                 idx, sqdist};
     if (e == cudaSuccess) {
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8));
+        qcell_count_kernel<<<g, 256, 0, s>>>(t->v, queries, (int)m, qcell, cnt);
+        const int nscan = scan_exclusive_u32(cnt, ncell + 1, scan_tmp, s);
+        qcell_scatter_kernel<<<g, 256, 0, s>>>(qcell, (int)m, cnt, perm);
+        count_launches(2 + nscan);
         switch (t->v.leaf_size) {
             case 4: e = launch_nn<4>(t->v, qs, (int)m, counter, s); break;
             case 8: e = launch_nn<8>(t->v, qs, (int)m, counter, s); break;
@@ -78,7 +118,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
             default: e = launch_nn<32>(t->v, qs, (int)m, counter, s); break;
         }
     }
-    cudaFreeAsync(counter, s);
+    cudaFreeAsync(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "nn_query_kernel launch");
     return CIL_OK;
 }

@@ -1,0 +1,100 @@
+// prim.cu -- device-wide primitives used by the index build and the query sort:
+// exclusive scan of uint32 (3 phases: tile sums, scan of tile sums, tile scans with carry).
+#include "internal.cuh"
+
+#include <algorithm>
+
+namespace cil {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;                          // per thread
+constexpr int kScanTile = kScanThreads * kScanItems;    // 4096 per block
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < kScanThreads / 32 ? warp_tot[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < kScanThreads / 32) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t wbase = w > 0 ? warp_tot[w - 1] : 0u;
+    if (total) *total = warp_tot[kScanThreads / 32 - 1];
+    __syncthreads();
+    return wbase + x - v;
+}
+
+__global__ void tile_sum_kernel(const uint32_t* __restrict__ a, int64_t len, uint32_t* __restrict__ tsum) {
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+        if (i < len) s += a[i];
+    }
+    uint32_t tot;
+    block_exclusive_scan(s, &tot);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+// exclusive scan of tsum[0..nt) in place, by one block (chunks of 256 with carry)
+__global__ void tile_prefix_kernel(uint32_t* __restrict__ tsum, int nt) {
+    uint32_t carry = 0;
+    for (int b = 0; b < nt; b += kScanThreads) {
+        const int i = b + threadIdx.x;
+        const uint32_t v = i < nt ? tsum[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan(v, &tot);
+        if (i < nt) tsum[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const uint32_t* __restrict__ tsum) {
+    // each thread owns kScanItems consecutive elements of the tile
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = base + k < len ? a[base + k] : 0u;
+        s += v[k];
+    }
+    uint32_t run = tsum[blockIdx.x] + block_exclusive_scan(s, nullptr);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < len) a[base + k] = run;
+        run += v[k];
+    }
+}
+
+}  // namespace
+
+size_t scan_temp_bytes(int64_t len) {
+    return align_up((size_t)((len + kScanTile - 1) / kScanTile) * 4, 256);
+}
+
+int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s) {
+    const int nt = (int)((len + kScanTile - 1) / kScanTile);
+    uint32_t* tsum = (uint32_t*)temp;
+    tile_sum_kernel<<<nt, kScanThreads, 0, s>>>(a, len, tsum);
+    tile_prefix_kernel<<<1, kScanThreads, 0, s>>>(tsum, nt);
+    tile_scan_kernel<<<nt, kScanThreads, 0, s>>>(a, len, tsum);
+    return 3;
+}
+
+}  // namespace cil

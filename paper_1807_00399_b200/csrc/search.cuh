@@ -195,15 +195,18 @@ __device__ __forceinline__ void ball_codes(const float4 Q, const DF3& s, float r
     chi = morton3(hx, hy, hz);
 }
 
-// Leaf whose first point is the first target of the query's coarse Morton cell (or the next
-// non-empty cell): a cold-start hint.
+// Cold-start hint: the leaf holding the target whose Morton key follows the query's own key
+// (coarse-cell table, then a binary search inside the query's coarse cell).
 __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& s) {
     const float4 Q = __ldg(T.quant);
     const unsigned long long code = morton_of(Q, s.hx, s.hy, s.hz);
     const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
-    int pos = (int)__ldg(T.cell_first + c);
-    pos = min(pos, T.n - 1);
-    return pos / T.leaf_size;
+    int lo = (int)__ldg(T.cell_first + c), hi = (int)__ldg(T.cell_first + c + 1);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(T.keys + mid) < code) lo = mid + 1; else hi = mid;
+    }
+    return min(lo, T.n - 1) / T.leaf_size;
 }
 
 // ---------------------------------------------------------------- per-lane search state
@@ -308,22 +311,82 @@ __device__ __forceinline__ int next_leaf(LaneSearch& L, LaneStack& K, const Targ
 
 // ---------------------------------------------------------------- warp-packet engine
 // A warp takes 32 consecutive queries (one per lane; consecutive = spatially coherent for
-// Morton- or scan-ordered inputs).  Phase 1: every lane evaluates its own hint leaf (its
-// warm-start match, or the coarse-cell hint), which gives each lane a tight bound.  Phase 2:
-// the warp walks the BVH together, top-down and nearest-first: a node is entered iff its box
-// lower bound is <= the best distance of at least one lane (ballot), so every lane sees every
-// node its own ball touches -- each lane's result is its exact nearest neighbour.  Box loads
-// are warp-uniform (broadcast), leaves are evaluated by all lanes with packed FP32, and the
-// DFS stack is held one entry per lane in a register, so control flow never diverges.
+// Morton- or scan-ordered inputs).
+//   A. every lane evaluates its own hint leaf (warm-start match or cold hint): a per-lane
+//      bound r_i = sqrt(best_i).
+//   B. lanes whose r_i is far above the packet mean are "outliers"; the others define the
+//      packet box P = AABB of their balls B(s_i, r_i) (conservatively inflated).
+//   C. breadth-first frontier walk of the BVH: children of the frontier are tested against P,
+//      one box per lane, and compacted with ballots; the last frontier is the list of leaves
+//      whose box meets P -- a superset of the leaves meeting any normal lane's ball.
+//   D. each candidate leaf is evaluated by all lanes (packed FP32) if its lower bound is <=
+//      the best distance of at least one lane.
+//   E. outlier lanes (and whole packets whose frontier overflowed) finish with the exact
+//      ballot DFS: a node is entered iff its lower bound is <= some active lane's best.
+// Every lane therefore examines every leaf that can hold a target inside its ball: each
+// lane's result is its exact nearest neighbour.
 // Q supplies
 //   __device__ bool load(int i, DF3& s, unsigned long long& init, int& hint_leaf)
 //   __device__ void store(int i, unsigned long long best, int bpos, const DF3& s)
+constexpr int kFrontierCap = 256;
+constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
+
+template <int B>
+__device__ __forceinline__ void ballot_dfs(const TargetView& T, const DF3& s, const NegQuery& nq, bool on,
+                                           unsigned long long& best, int& bpos) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int l_pad = T.l_pad;
+    // lanes that are not searching use a negative radius: no lower bound can pass it
+    const float neg = -1.0f;
+    int stk = 0, sp = 0, v = 1;
+    while (true) {
+        const float bd = on ? key_d2(best) : neg;
+        if (v >= l_pad) {
+            eval_leaf<B>(T, nq, v - l_pad, best, bpos);
+        } else {
+            const int c = 2 * v;
+            const float4* bx = T.box + 2 * (size_t)c;
+            const float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
+            const float lb0 = box_lb2(s, lo0, hi0), lb1 = box_lb2(s, lo1, hi1);
+            const unsigned m0 = __ballot_sync(FULL, lb0 <= bd);
+            const unsigned m1 = __ballot_sync(FULL, lb1 <= bd);
+            if (m0 && m1) {
+                const unsigned pref1 = __ballot_sync(FULL, lb1 < lb0);
+                const bool right_first = __popc(pref1 & (m0 | m1)) * 2 > __popc(m0 | m1);
+                if (lane == sp) stk = right_first ? c : c + 1;
+                ++sp;
+                v = right_first ? c + 1 : c;
+                continue;
+            }
+            if (m0) { v = c; continue; }
+            if (m1) { v = c + 1; continue; }
+        }
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            const int cand = __shfl_sync(FULL, stk, sp);
+            const float lb = node_lb2(T, s, cand);
+            if (__any_sync(FULL, lb <= (on ? key_d2(best) : neg))) { v = cand; found = true; break; }
+        }
+        if (!found) break;
+    }
+}
+
+__device__ __forceinline__ bool box_meets(float4 lo, float4 hi, float4 plo, float4 phi) {
+    return lo.x <= phi.x && lo.y <= phi.y && lo.z <= phi.z && hi.x >= plo.x && hi.y >= plo.y && hi.z >= plo.z;
+}
+
 template <int B, class Q, class Stats = NoStats>
 __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int m, unsigned int* counter,
                                                  Stats* st = nullptr) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const int l_pad = T.l_pad;
+    __shared__ int frontier[kEngineWarps][2][kFrontierCap];
+    int* F = frontier[threadIdx.x >> 5][0];
+    int* G = frontier[threadIdx.x >> 5][1];
     while (true) {
         int base = 0;
         if (lane == 0) base = (int)atomicAdd(counter, 32u);
@@ -339,55 +402,87 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             active = qs.load(qi, s, best, hint);
             if (active && hint < 0) hint = coarse_hint_leaf(T, s);
         }
-        if (!active) {            // inactive lanes: a point far away that never asks for a node
-            s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f;
-            best = make_key(-1.0f, 0u);   // negative radius: every lower bound exceeds it
-        }
+        if (!active) { s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f; }
         const NegQuery nq = neg_query(s);
+        // ---- A
         if (active) {
             if (st) st->leaf();
             eval_leaf<B>(T, nq, hint, best, bpos);
         }
-        // phase 2: converged top-down traversal
-        int stk = 0;              // lane k holds stack entry k
-        int sp = 0;               // warp-uniform stack depth
-        int v = 1;
-        while (true) {
-            if (v >= l_pad) {
-                if (st) st->leaf();
-                eval_leaf<B>(T, nq, v - l_pad, best, bpos);
-            } else {
-                if (st) st->node();
-                const int c = 2 * v;
-                const float4* bx = T.box + 2 * (size_t)c;
-                const float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
-                const float bd = key_d2(best);
-                const float lb0 = box_lb2(s, lo0, hi0), lb1 = box_lb2(s, lo1, hi1);
-                const unsigned m0 = __ballot_sync(FULL, lb0 <= bd);
-                const unsigned m1 = __ballot_sync(FULL, lb1 <= bd);
-                if (m0 && m1) {
-                    // nearer child first: the one more lanes prefer
-                    const unsigned pref1 = __ballot_sync(FULL, lb1 < lb0);
-                    const bool right_first = __popc(pref1 & (m0 | m1)) * 2 > __popc(m0 | m1);
-                    const int far_ = right_first ? c : c + 1;
-                    if (lane == sp) stk = far_;
-                    ++sp;
-                    v = right_first ? c + 1 : c;
-                    continue;
-                }
-                if (m0) { v = c; continue; }
-                if (m1) { v = c + 1; continue; }
-            }
-            // pop, skipping subtrees no lane needs any more
-            bool found = false;
-            while (sp > 0) {
-                --sp;
-                const int cand = __shfl_sync(FULL, stk, sp);
-                const float lb = node_lb2(T, s, cand);
-                if (__any_sync(FULL, lb <= key_d2(best))) { v = cand; found = true; break; }
-            }
-            if (!found) break;
+        // ---- B: outliers and the packet box
+        const float r = active ? sqrtf(key_d2(best)) : 0.0f;
+        float rsum = r;
+        int na = active ? 1 : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            rsum += __shfl_xor_sync(FULL, rsum, o);
+            na += __shfl_xor_sync(FULL, na, o);
         }
+        const float rcap = 3.0f * rsum / (float)max(na, 1);
+        const bool normal = active && r <= rcap && r < INFINITY;
+        const bool outlier = active && !normal;
+        // inflate for the double-float offset and for rounding of s_hi -/+ r
+        const float rx = r * 1.000001f + fabsf(s.lx) + 1e-6f * fabsf(s.hx) + 1e-30f;
+        const float ry = r * 1.000001f + fabsf(s.ly) + 1e-6f * fabsf(s.hy) + 1e-30f;
+        const float rz = r * 1.000001f + fabsf(s.lz) + 1e-6f * fabsf(s.hz) + 1e-30f;
+        float4 plo = make_float4(normal ? s.hx - rx : INFINITY, normal ? s.hy - ry : INFINITY,
+                                 normal ? s.hz - rz : INFINITY, 0.0f);
+        float4 phi = make_float4(normal ? s.hx + rx : -INFINITY, normal ? s.hy + ry : -INFINITY,
+                                 normal ? s.hz + rz : -INFINITY, 0.0f);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            plo.x = fminf(plo.x, __shfl_xor_sync(FULL, plo.x, o));
+            plo.y = fminf(plo.y, __shfl_xor_sync(FULL, plo.y, o));
+            plo.z = fminf(plo.z, __shfl_xor_sync(FULL, plo.z, o));
+            phi.x = fmaxf(phi.x, __shfl_xor_sync(FULL, phi.x, o));
+            phi.y = fmaxf(phi.y, __shfl_xor_sync(FULL, phi.y, o));
+            phi.z = fmaxf(phi.z, __shfl_xor_sync(FULL, phi.z, o));
+        }
+        bool overflow = false;
+        if (__any_sync(FULL, normal)) {
+            // ---- C: frontier walk from the root against the packet box
+            if (lane == 0) F[0] = 1;
+            __syncwarp();
+            int nF = 1;
+            for (int lev = 0; lev < T.levels && nF > 0; ++lev) {
+                const int nC = 2 * nF;
+                int nN = 0;
+                for (int b0 = 0; b0 < nC; b0 += 32) {
+                    const int j = b0 + lane;
+                    int c = 0;
+                    bool hit = false;
+                    if (j < nC) {
+                        c = 2 * F[j >> 1] + (j & 1);
+                        const float4* bx = T.box + 2 * (size_t)c;
+                        hit = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
+                    }
+                    const unsigned mk = __ballot_sync(FULL, hit);
+                    const int pos = nN + __popc(mk & lt);
+                    if (hit && pos < kFrontierCap) G[pos] = c;
+                    nN += __popc(mk);
+                }
+                __syncwarp();
+                if (st && lane == 0) st->node();
+                if (nN > kFrontierCap) { overflow = true; break; }
+                int* tmp = F; F = G; G = tmp;
+                nF = nN;
+            }
+            // ---- D: candidate leaves
+            if (!overflow) {
+                for (int k = 0; k < nF; ++k) {
+                    const int v = F[k];
+                    const float lb = node_lb2(T, s, v);
+                    if (__any_sync(FULL, normal && lb <= key_d2(best))) {
+                        if (st) st->leaf();
+                        eval_leaf<B>(T, nq, v - l_pad, best, bpos);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // ---- E: exact ballot DFS for outliers (or everyone after an overflow)
+        const bool dfs_on = outlier || (overflow && normal);
+        if (__any_sync(FULL, dfs_on)) ballot_dfs<B>(T, s, nq, dfs_on, best, bpos);
         if (active) qs.store(qi, best, bpos, s);
     }
 }

@@ -5,10 +5,12 @@
 //
 // Pipeline (all hand-written kernels, one stream, no host synchronisation):
 //   K1a bbox partials -> K1b bbox final -> K1c 48-bit Morton key per point
-//   K2  stable LSD radix sort of (key, index) (6 passes x 8 bits: histogram, scan, scatter)
+//   K2  stable LSD radix sort of (key, index) (6 passes x 8 bits: histogram, 3-phase scan,
+//       stable warp-ranked scatter)
 //   K4  gather: sorted float4 (x, y, z, orig index) points and float4 normals
-//   K5  leaf AABBs (leaf_size consecutive sorted points), then internal AABBs level by level
-//       of an implicit complete binary tree (node v has children 2v, 2v+1).
+//   K5  leaf AABBs (leaf_size consecutive sorted points) and SoA leaf blocks, then internal
+//       AABBs of an implicit complete binary tree (node v has children 2v, 2v+1), 8 levels per
+//       shared-memory pass; K6 coarse-cell table (first sorted index of every coarse cell).
 #include "internal.cuh"
 #include "search.cuh"
 
@@ -55,18 +57,32 @@ __global__ void bbox_partial_kernel(const float* __restrict__ p, int n, float* _
     }
 }
 
-// quant = (min.x, min.y, min.z, cells per unit)
+// quant = (min.x, min.y, min.z, cells per unit); one block of kThreads
 __global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, float4* __restrict__ quant) {
-    if (threadIdx.x != 0) return;
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
-    for (int b = 0; b < nblk; ++b)
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x)
         for (int a = 0; a < 3; ++a) {
             mn[a] = fminf(mn[a], part[6 * b + a]);
             mx[a] = fmaxf(mx[a], part[6 * b + 3 + a]);
         }
-    float ext = fmaxf(fmaxf(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
-    float cells = (float)((1 << kMortonBits) - 1);
-    *quant = make_float4(mn[0], mn[1], mn[2], ext > 0.0f ? cells / ext : 0.0f);
+    __shared__ float sm[6][kThreads / 32];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        for (int o = 16; o; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0)
+        for (int a = 0; a < 3; ++a) { sm[a][w] = mn[a]; sm[3 + a][w] = mx[a]; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kThreads / 32; ++k)
+            for (int a = 0; a < 3; ++a) { sm[a][0] = fminf(sm[a][0], sm[a][k]); sm[3 + a][0] = fmaxf(sm[3 + a][0], sm[3 + a][k]); }
+        const float ext = fmaxf(fmaxf(sm[3][0] - sm[0][0], sm[4][0] - sm[1][0]), sm[5][0] - sm[2][0]);
+        const float cells = (float)((1 << kMortonBits) - 1);
+        *quant = make_float4(sm[0][0], sm[1][0], sm[2][0], ext > 0.0f ? cells / ext : 0.0f);
+    }
 }
 
 __global__ void morton_kernel(const float* __restrict__ p, int n, const float4* __restrict__ quant,
@@ -100,30 +116,6 @@ __global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, i
     }
     __syncthreads();
     for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(size_t)d * nblk + blockIdx.x] = h[d];
-}
-
-// in-place exclusive scan of `len` counters with one block of 1024 threads
-__global__ void scan_kernel(uint32_t* __restrict__ a, int len) {
-    __shared__ uint32_t part[1024];
-    const int t = threadIdx.x;
-    const int per = (len + 1023) / 1024;
-    const int beg = t * per, end = min(beg + per, len);
-    uint32_t s = 0;
-    for (int i = beg; i < end; ++i) s += a[i];
-    part[t] = s;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        uint32_t v = t >= o ? part[t - o] : 0u;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
-    }
-    uint32_t run = part[t] - s;   // exclusive prefix of this thread's chunk
-    for (int i = beg; i < end; ++i) {
-        uint32_t v = a[i];
-        a[i] = run;
-        run += v;
-    }
 }
 
 // stable scatter: within a tile, warp w owns keys [w*512, (w+1)*512) processed in rounds of 32
@@ -215,25 +207,48 @@ __global__ void leaf_soa_kernel(const float4* __restrict__ pts, int n, int B, in
     }
 }
 
-// nodes [first, 2*first) from their children
-__global__ void level_box_kernel(float4* __restrict__ box, int first) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < first; k += gridDim.x * blockDim.x) {
-        const size_t v = (size_t)first + k, c = 2 * v;
-        float4 l0 = box[2 * c], h0 = box[2 * c + 1], l1 = box[2 * c + 2], h1 = box[2 * c + 3];
-        box[2 * v] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.0f);
-        box[2 * v + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.0f);
+// cell_first[c] = first sorted index whose key >> shift >= c, for c in [0, ncell] (binary search)
+__global__ void cell_first_kernel(const unsigned long long* __restrict__ keys, int n, int shift, uint32_t ncell,
+                                  uint32_t* __restrict__ cell_first) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= (int64_t)ncell;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)c << shift;
+        int lo = 0, hi = n;                    // first index with keys[i] >= key
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (keys[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        cell_first[c] = (uint32_t)lo;
     }
 }
 
-// cell_first[c] = first sorted index whose key >> shift >= c, for c in [0, ncell]
-__global__ void cell_first_kernel(const unsigned long long* __restrict__ keys, int n, int shift, uint32_t ncell,
-                                  uint32_t* __restrict__ cell_first) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const long long c = (long long)(keys[i] >> shift);
-        const long long cp = i > 0 ? (long long)(keys[i - 1] >> shift) : -1;
-        for (long long q = cp + 1; q <= c; ++q) cell_first[q] = (uint32_t)i;
-        if (i == n - 1)
-            for (long long q = c + 1; q <= (long long)ncell; ++q) cell_first[q] = (uint32_t)n;
+// Internal node boxes, 8 levels per pass: block b reduces nodes [first + 256 b, first + 256 (b+1))
+// of the current bottom level up `lv` levels, through shared memory.
+constexpr int kPassNodes = 256;
+__global__ void tree_pass_kernel(float4* __restrict__ box, int first, int lv) {
+    __shared__ float4 slo[kPassNodes], shi[kPassNodes];
+    const int t = threadIdx.x;
+    const int width = min(kPassNodes, first);          // nodes per block at the bottom level
+    const int v0 = first + blockIdx.x * width;
+    if (t < width) { slo[t] = box[2 * (size_t)(v0 + t)]; shi[t] = box[2 * (size_t)(v0 + t) + 1]; }
+    __syncthreads();
+    int cnt = width;
+    for (int j = 1; j <= lv; ++j) {
+        cnt >>= 1;
+        float4 lo, hi;
+        if (t < cnt) {
+            const float4 l0 = slo[2 * t], l1 = slo[2 * t + 1], h0 = shi[2 * t], h1 = shi[2 * t + 1];
+            lo = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.0f);
+            hi = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.0f);
+        }
+        __syncthreads();
+        if (t < cnt) {
+            slo[t] = lo; shi[t] = hi;
+            const size_t v = (size_t)(v0 >> j) + t;
+            box[2 * v] = lo;
+            box[2 * v + 1] = hi;
+        }
+        __syncthreads();
     }
 }
 
@@ -306,7 +321,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     const size_t s_keys = align_up((size_t)N * 8, 256), s_vals = align_up((size_t)N * 4, 256);
     const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
     const size_t s_bb = align_up((size_t)(6 * nblk_bbox) * 4, 256);
-    const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb;
+    const size_t s_scan = scan_temp_bytes((int64_t)kRadix * nblk_sort);
+    const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb + s_scan;
     void* tmp = nullptr;
     cudaError_t e = cudaMallocAsync(&tmp, scratch, s);
     if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cudaMallocAsync(scratch)"); }
@@ -317,29 +333,33 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     uint32_t* v1 = (uint32_t*)(tb + 2 * s_keys + s_vals);
     uint32_t* hist = (uint32_t*)(tb + 2 * s_keys + 2 * s_vals);
     float* bbp = (float*)(tb + 2 * s_keys + 2 * s_vals + s_hist);
+    void* scan_tmp = (void*)(tb + 2 * s_keys + 2 * s_vals + s_hist + s_bb);
+    int nlaunch = 0;
 
     bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, N, bbp);
-    bbox_final_kernel<<<1, 32, 0, s>>>(bbp, nblk_bbox, d_quant);
+    bbox_final_kernel<<<1, kThreads, 0, s>>>(bbp, nblk_bbox, d_quant);
     morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, d_quant, k0, v0);
     for (int shift = 0; shift < 3 * kMortonBits; shift += kRadixBits) {
         radix_hist_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, N, shift, hist, nblk_sort);
-        scan_kernel<<<1, 1024, 0, s>>>(hist, kRadix * nblk_sort);
+        nlaunch += scan_exclusive_u32(hist, (int64_t)kRadix * nblk_sort, scan_tmp, s);
         radix_scatter_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, v0, k1, v1, N, shift, hist, nblk_sort);
         std::swap(k0, k1);
         std::swap(v0, v1);
     }
     gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, d_pts, d_nrm);
     cudaMemcpyAsync(d_keys, k0, (size_t)N * 8, cudaMemcpyDeviceToDevice, s);
-    cell_first_kernel<<<grid_for(N), kThreads, 0, s>>>(k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
+    cell_first_kernel<<<grid_for(ncell + 1), kThreads, 0, s>>>(k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
     leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(d_pts, N, B, (int)l_pad, d_box);
     leaf_soa_kernel<<<grid_for(n_leaves * B), kThreads, 0, s>>>(d_pts, N, B, n_leaves, d_soa);
-    for (int64_t first = l_pad / 2; first >= 1; first /= 2)
-        level_box_kernel<<<grid_for(first), kThreads, 0, s>>>(d_box, (int)first);
-    {
-        int levels = 0;
-        for (int64_t f = l_pad / 2; f >= 1; f /= 2) ++levels;
-        count_launches(3 + 3 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + 4 + levels);
+    int tree_passes = 0;
+    for (int first = (int)l_pad, rem = levels; rem > 0; ++tree_passes) {
+        const int lv = std::min(rem, 8);
+        const int width = std::min(kPassNodes, first);
+        tree_pass_kernel<<<first / width, kPassNodes, 0, s>>>(d_box, first, lv);
+        first >>= lv;
+        rem -= lv;
     }
+    count_launches(3 + 2 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + nlaunch + 4 + tree_passes);
     e = cudaGetLastError();
     cudaFreeAsync(tmp, s);
     if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cil_target_build launch"); }

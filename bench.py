@@ -80,7 +80,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -156,6 +156,8 @@ def run_ours(args, rank, world, local_rank):
     # timed region: K steps, L2 flushed before each; events on the launching stream
     launches0 = cil.launch_count()
     tot_ms, build_ms, run_ms = 0.0, 0.0, 0.0
+    cil.profile_read()
+    cil.profile_enable(True)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -172,6 +174,8 @@ def run_ours(args, rank, world, local_rank):
             build_ms += evs[0].elapsed_time(evs[1])
             run_ms += evs[1].elapsed_time(evs[2])
         torch.cuda.synchronize()
+    cil.profile_enable(False)
+    prof = cil.profile_read()
     launches = cil.launch_count() - launches0
     if world > 1:
         import torch.distributed as dist
@@ -189,9 +193,12 @@ def run_ours(args, rank, world, local_rank):
         return None
     ms_step = tot_max / args.steps
     value = total_pairs / (tot_max / 1e3)
-    # dominant kernel: the fused iteration; its average launch = run time / iterations
-    # (run = init + iters x icp_iter_kernel + final, so this slightly overstates the launch)
-    it_ms = (run_ms / args.steps) / iters
+    # dominant unit: one ICP iteration = icp_nn_kernel (correspondences) + icp_acc_kernel
+    # (transform/reject/J^TJ/J^Tr/reduce/solve), each launch timed with CUDA events on the
+    # launching stream inside the timed region (library profiler)
+    nn_ms = prof["nn_ms"] / max(prof["n_nn"], 1)
+    acc_ms = prof["acc_ms"] / max(prof["n_acc"], 1)
+    it_ms = nn_ms + acc_ms
     bpp = _bytes_per_pair(metric)
     achieved = bpp * w.m / (it_ms * 1e-3) / 1e9
     peak, peak_src = _peak_hbm()
@@ -210,10 +217,13 @@ def run_ours(args, rank, world, local_rank):
             "n_target": w.n, "n_source": w.m, "iterations": iters, "leaf_size": args.leaf or 8,
             "l2": "flushed before every step (512 MiB device write)",
             "build_ms": build_ms / args.steps, "icp_ms_per_iteration": it_ms,
+            "icp_nn_kernel_ms": nn_ms, "icp_acc_kernel_ms": acc_ms, "run_ms": run_ms / args.steps,
+            "timed_launches": {"nn": prof["n_nn"], "acc": prof["n_acc"], "build": prof["n_build"]},
             "final_status": r.status, "final_n_corr": r.n_corr, "final_rmse": r.rmse,
             "parallelism": f"independent frame pair per rank x{world}",
         },
-        "roofline": {"bound": "hbm", "kernel": "icp_iter_kernel", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "icp_nn_kernel+icp_acc_kernel (one ICP iteration)",
+                     "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_pair": bpp, "peak_source": peak_src,
                      "frac_of_8TBps_nominal": achieved / 8000.0},
@@ -340,7 +350,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4_plane")

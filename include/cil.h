@@ -191,6 +191,18 @@ const char* cil_version(void);
    (host counter, incremented at every launch). */
 uint64_t cil_launch_count(void);
 
+/* Diagnostics: per-launch CUDA-event timing.  While enabled, the library records a CUDA
+   event pair on the launching stream around every cil_target_build call and every
+   correspondence (K_nn), accumulation (K_acc) and nn_query launch.  cil_profile_read
+   synchronises those events, adds their durations per class into *out and clears the list.
+   Host-only API; not thread-safe. */
+typedef struct {
+    double build_ms, nn_ms, acc_ms, query_ms;   /* summed event durations */
+    int64_t n_build, n_nn, n_acc, n_query;       /* number of timed launches */
+} cil_profile_stats;
+cil_status cil_profile_enable(int on);
+cil_status cil_profile_read(cil_profile_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

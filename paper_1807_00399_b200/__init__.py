@@ -43,7 +43,7 @@ METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_
 
 EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
-            "cil_last_error", "cil_version", "cil_launch_count"]
+            "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read"]
 
 
 class cil_index_params(C.Structure):
@@ -64,6 +64,11 @@ class cil_icp_result(C.Structure):
 class cil_icp_system(C.Structure):
     _fields_ = [("H", C.c_double * 36), ("g", C.c_double * 6), ("x", C.c_double * 6), ("sse", C.c_double),
                 ("n_corr", C.c_int64), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+class cil_profile_stats(C.Structure):
+    _fields_ = [("build_ms", C.c_double), ("nn_ms", C.c_double), ("acc_ms", C.c_double), ("query_ms", C.c_double),
+                ("n_build", C.c_int64), ("n_nn", C.c_int64), ("n_acc", C.c_int64), ("n_query", C.c_int64)]
 
 
 class cil_target_info(C.Structure):
@@ -91,6 +96,23 @@ _lib.cil_status_string.argtypes = [C.c_int]
 _lib.cil_last_error.restype = C.c_char_p
 _lib.cil_version.restype = C.c_char_p
 _lib.cil_launch_count.restype = C.c_uint64
+
+
+_lib.cil_profile_enable.restype = C.c_int
+_lib.cil_profile_enable.argtypes = [C.c_int]
+_lib.cil_profile_read.restype = C.c_int
+_lib.cil_profile_read.argtypes = [C.POINTER(cil_profile_stats)]
+
+
+def profile_enable(on: bool = True) -> None:
+    """per-launch CUDA-event timing inside the library (diagnostics)"""
+    _check(_lib.cil_profile_enable(1 if on else 0), "cil_profile_enable")
+
+
+def profile_read() -> dict:
+    st = cil_profile_stats()
+    _check(_lib.cil_profile_read(C.byref(st)), "cil_profile_read")
+    return {k: getattr(st, k) for k, _ in cil_profile_stats._fields_}
 
 
 def launch_count() -> int:

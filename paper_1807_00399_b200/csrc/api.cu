@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <cstring>
+#include <vector>
 
 namespace cil {
 
@@ -13,6 +14,33 @@ std::atomic<unsigned long long> g_launches{0};
 }  // namespace
 
 void count_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec { int cls; cudaEvent_t a, b; };
+bool g_prof = false;
+std::vector<cudaEvent_t> g_pool;
+std::vector<ProfRec> g_recs;
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+bool prof_on() { return g_prof; }
+
+void prof_begin(int cls, cudaStream_t s) {
+    if (!g_prof) return;
+    ProfRec r{cls, take_event(), take_event()};
+    cudaEventRecord(r.a, s);
+    g_recs.push_back(r);
+}
+
+void prof_end(cudaStream_t s) {
+    if (!g_prof || g_recs.empty()) return;
+    cudaEventRecord(g_recs.back().b, s);
+}
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -50,6 +78,31 @@ CIL_API const char* cil_status_string(cil_status s) {
 }
 
 CIL_API const char* cil_last_error(void) { return cil::g_err; }
+
+CIL_API cil_status cil_profile_enable(int on) {
+    cil::g_prof = on != 0;
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_profile_read(cil_profile_stats* out) {
+    if (!out) return CIL_ERR_INVALID_ARG;
+    std::memset(out, 0, sizeof(*out));
+    for (auto& r : cil::g_recs) {
+        float ms = 0.0f;
+        cudaEventSynchronize(r.b);
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) ms = 0.0f;
+        switch (r.cls) {
+            case cil::kProfBuild: out->build_ms += ms; ++out->n_build; break;
+            case cil::kProfNN: out->nn_ms += ms; ++out->n_nn; break;
+            case cil::kProfAcc: out->acc_ms += ms; ++out->n_acc; break;
+            default: out->query_ms += ms; ++out->n_query; break;
+        }
+        cil::g_pool.push_back(r.a);
+        cil::g_pool.push_back(r.b);
+    }
+    cil::g_recs.clear();
+    return CIL_OK;
+}
 
 CIL_API uint64_t cil_launch_count(void) { return (uint64_t)cil::g_launches.load(); }
 

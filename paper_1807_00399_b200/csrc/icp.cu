@@ -386,7 +386,9 @@ template <int B>
 cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
     static const int occ = occupancy_of(icp_nn_kernel<B>, kNNThreads);
     const int g = persistent_grid(occ, kNNThreads, a.m, 1 << 20);
+    prof_begin(kProfNN, s);
     icp_nn_kernel<B><<<g, kNNThreads, 0, s>>>(a);
+    prof_end(s);
     return cudaGetLastError();
 }
 
@@ -394,7 +396,9 @@ template <int METRIC>
 cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
     static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads);
     const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
+    prof_begin(kProfAcc, s);
     icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
+    prof_end(s);
     return cudaGetLastError();
 }
 

@@ -68,6 +68,12 @@ inline cil_status cuda_fail(cudaError_t e, const char* what) {
 int sm_count();            // of the current device (cached per device)
 void count_launches(int k);   // diagnostics counter behind cil_launch_count()
 
+// diagnostics: per-launch event timing (cil_profile_*)
+enum ProfClass { kProfBuild = 0, kProfNN = 1, kProfAcc = 2, kProfQuery = 3 };
+bool prof_on();
+void prof_begin(int cls, cudaStream_t s);   // records the start event of a timed region
+void prof_end(cudaStream_t s);              // records the end event
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)

@@ -102,6 +102,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     uint32_t* qcell = (uint32_t*)(sb + 256 + b_cnt);
     uint32_t* perm = (uint32_t*)(sb + 256 + b_cnt + b_q);
     void* scan_tmp = (void*)(sb + 256 + b_cnt + 2 * b_q);
+    prof_begin(kProfQuery, s);
     cudaError_t e = cudaMemsetAsync(sb, 0, 256 + b_cnt, s);
     NNQueries qs{queries, perm, std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist),
                  idx, sqdist};
@@ -118,6 +119,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
             default: e = launch_nn<32>(t->v, qs, (int)m, counter, s); break;
         }
     }
+    prof_end(s);
     cudaFreeAsync(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "nn_query_kernel launch");
     return CIL_OK;

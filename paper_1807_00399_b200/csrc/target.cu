@@ -336,6 +336,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     void* scan_tmp = (void*)(tb + 2 * s_keys + 2 * s_vals + s_hist + s_bb);
     int nlaunch = 0;
 
+    prof_begin(kProfBuild, s);
     bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, N, bbp);
     bbox_final_kernel<<<1, kThreads, 0, s>>>(bbp, nblk_bbox, d_quant);
     morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, d_quant, k0, v0);
@@ -360,6 +361,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
         rem -= lv;
     }
     count_launches(3 + 2 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + nlaunch + 4 + tree_passes);
+    prof_end(s);
     e = cudaGetLastError();
     cudaFreeAsync(tmp, s);
     if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cil_target_build launch"); }

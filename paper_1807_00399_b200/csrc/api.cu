@@ -28,6 +28,32 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
+namespace {
+cudaMemPool_t g_pool_dev[64] = {};
+}  // namespace
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+    if (!g_pool_dev[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        e = cudaMemPoolCreate(&pool, &props);
+        if (e != cudaSuccess) return e;
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool_dev[dev] = pool;
+    }
+    return cudaMallocFromPoolAsync(p, bytes, g_pool_dev[dev], s);
+}
+
+cudaError_t pool_free(void* p, cudaStream_t s) { return cudaFreeAsync(p, s); }
+
 bool prof_on() { return g_prof; }
 
 void prof_begin(int cls, cudaStream_t s) {

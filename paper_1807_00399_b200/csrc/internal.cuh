@@ -66,6 +66,10 @@ inline cil_status cuda_fail(cudaError_t e, const char* what) {
     return e == cudaErrorMemoryAllocation ? CIL_ERR_OOM : CIL_ERR_CUDA;
 }
 int sm_count();            // of the current device (cached per device)
+// stream-ordered allocation from the library's own pool (release threshold: never trim, so
+// repeated builds/queries after a synchronize do not re-map memory)
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s);
+cudaError_t pool_free(void* p, cudaStream_t s);
 void count_launches(int k);   // diagnostics counter behind cil_launch_count()
 
 // diagnostics: per-launch event timing (cil_profile_*)

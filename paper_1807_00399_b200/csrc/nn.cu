@@ -95,7 +95,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     const size_t b_q = align_up((size_t)m * 4, 256);
     const size_t b_scan = scan_temp_bytes(ncell + 1);
     void* scratch = nullptr;
-    CIL_CUDA_TRY(cudaMallocAsync(&scratch, 256 + b_cnt + 2 * b_q + b_scan, s), "cudaMallocAsync(nn scratch)");
+    CIL_CUDA_TRY(pool_alloc(&scratch, 256 + b_cnt + 2 * b_q + b_scan, s), "pool_alloc(nn scratch)");
     char* sb = (char*)scratch;
     unsigned int* counter = (unsigned int*)sb;
     uint32_t* cnt = (uint32_t*)(sb + 256);
@@ -120,7 +120,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
         }
     }
     prof_end(s);
-    cudaFreeAsync(scratch, s);
+    pool_free(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "nn_query_kernel launch");
     return CIL_OK;
 }

@@ -168,14 +168,19 @@ __device__ __forceinline__ void eval_leaf(const TargetView& T, const NegQuery& q
 #pragma unroll
     for (int c = 1; c < B; ++c) mn = fminf(mn, d2[c]);
     if (mn <= key_d2(best)) {                                   // an improvement or a tie is possible
+        // lowest original index among the candidates at the minimum (R1), then one key compare
         const int* ids = reinterpret_cast<const int*>(blk + 3 * R);
+        uint32_t imin = 0xffffffffu;
+        int cmin = 0;
 #pragma unroll
         for (int c = 0; c < B; ++c) {
-            if (d2[c] == mn) {
-                const unsigned long long k = make_key(mn, (uint32_t)__ldg(ids + c));
-                if (k < best) { best = k; bpos = leaf * B + c; }
-            }
+            const uint32_t id = (uint32_t)__ldg(ids + c);
+            const bool take = d2[c] == mn && id < imin;
+            imin = take ? id : imin;
+            cmin = take ? c : cmin;
         }
+        const unsigned long long k = make_key(mn, imin);
+        if (k < best) { best = k; bpos = leaf * B + cmin; }
     }
 }
 
@@ -319,8 +324,10 @@ __device__ __forceinline__ int next_leaf(LaneSearch& L, LaneStack& K, const Targ
 //   C. breadth-first frontier walk of the BVH: children of the frontier are tested against P,
 //      one box per lane, and compacted with ballots; the last frontier is the list of leaves
 //      whose box meets P -- a superset of the leaves meeting any normal lane's ball.
-//   D. each candidate leaf is evaluated by all lanes (packed FP32) if its lower bound is <=
-//      the best distance of at least one lane.
+//   D. every lane tests every candidate leaf's box against its own ball and appends the
+//      leaves it needs to a private work list (shared memory); the lists are then evaluated in
+//      rounds, each lane gathering its own leaf (packed FP32), so the number of evaluation
+//      rounds is the longest list, not the size of the packet's union.
 //   E. outlier lanes (and whole packets whose frontier overflowed) finish with the exact
 //      ballot DFS: a node is entered iff its lower bound is <= some active lane's best.
 // Every lane therefore examines every leaf that can hold a target inside its ball: each
@@ -329,6 +336,7 @@ __device__ __forceinline__ int next_leaf(LaneSearch& L, LaneStack& K, const Targ
 //   __device__ bool load(int i, DF3& s, unsigned long long& init, int& hint_leaf)
 //   __device__ void store(int i, unsigned long long best, int bpos, const DF3& s)
 constexpr int kFrontierCap = 256;
+constexpr int kListCap = 8;         // per-lane work-list entries before an evaluation batch
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
 template <int B>
@@ -385,6 +393,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
     const unsigned lt = (1u << lane) - 1u;
     const int l_pad = T.l_pad;
     __shared__ int frontier[kEngineWarps][2][kFrontierCap];
+    __shared__ int worklist[kEngineWarps][1][kListCap * 32];
     int* F = frontier[threadIdx.x >> 5][0];
     int* G = frontier[threadIdx.x >> 5][1];
     while (true) {
@@ -467,14 +476,26 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                 int* tmp = F; F = G; G = tmp;
                 nF = nN;
             }
-            // ---- D: candidate leaves
+            // ---- D: candidate leaves -> per-lane work lists -> gather-evaluation rounds
             if (!overflow) {
+                int* wl = worklist[threadIdx.x >> 5][0];   // [kListCap][32], lane-major
+                int cnt = 0;
                 for (int k = 0; k < nF; ++k) {
                     const int v = F[k];
                     const float lb = node_lb2(T, s, v);
-                    if (__any_sync(FULL, normal && lb <= key_d2(best))) {
-                        if (st) st->leaf();
-                        eval_leaf<B>(T, nq, v - l_pad, best, bpos);
+                    const bool need = normal && lb <= key_d2(best);
+                    if (need) { wl[cnt * 32 + lane] = v - l_pad; ++cnt; }
+                    if (__any_sync(FULL, cnt == kListCap) || k == nF - 1) {
+                        int rounds = cnt;
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) rounds = max(rounds, __shfl_xor_sync(FULL, rounds, o));
+                        for (int q = 0; q < rounds; ++q) {
+                            if (q < cnt) {
+                                if (st) st->leaf();
+                                eval_leaf<B>(T, nq, wl[q * 32 + lane], best, bpos);
+                            }
+                        }
+                        cnt = 0;
                     }
                 }
             }

@@ -305,7 +305,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     int dev = 0;
     CIL_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
     void* mem = nullptr;
-    CIL_CUDA_TRY(cudaMallocAsync(&mem, bytes, s), "cudaMallocAsync(target)");
+    CIL_CUDA_TRY(pool_alloc(&mem, bytes, s), "pool_alloc(target)");
     char* base = (char*)mem;
     float4* d_pts = (float4*)base;
     float4* d_nrm = normals ? (float4*)(base + b_pts) : nullptr;
@@ -324,8 +324,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     const size_t s_scan = scan_temp_bytes((int64_t)kRadix * nblk_sort);
     const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb + s_scan;
     void* tmp = nullptr;
-    cudaError_t e = cudaMallocAsync(&tmp, scratch, s);
-    if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cudaMallocAsync(scratch)"); }
+    cudaError_t e = pool_alloc(&tmp, scratch, s);
+    if (e != cudaSuccess) { pool_free(mem, s); return cuda_fail(e, "pool_alloc(scratch)"); }
     char* tb = (char*)tmp;
     unsigned long long* k0 = (unsigned long long*)tb;
     unsigned long long* k1 = (unsigned long long*)(tb + s_keys);
@@ -363,8 +363,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     count_launches(3 + 2 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + nlaunch + 4 + tree_passes);
     prof_end(s);
     e = cudaGetLastError();
-    cudaFreeAsync(tmp, s);
-    if (e != cudaSuccess) { cudaFreeAsync(mem, s); return cuda_fail(e, "cil_target_build launch"); }
+    pool_free(tmp, s);
+    if (e != cudaSuccess) { pool_free(mem, s); return cuda_fail(e, "cil_target_build launch"); }
 
     cil_target* t = new cil_target;
     t->v.pts = d_pts;
@@ -390,9 +390,9 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
 
 CIL_API cil_status cil_target_free(cil_target* t, cil_stream_t stream) {
     if (!t) return CIL_OK;
-    cudaError_t e = cudaFreeAsync(t->mem, (cudaStream_t)stream);
+    cudaError_t e = pool_free(t->mem, (cudaStream_t)stream);
     delete t;
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(target)");
+    if (e != cudaSuccess) return cuda_fail(e, "pool_free(target)");
     return CIL_OK;
 }
 

@@ -174,6 +174,13 @@ cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_t m, con
 /* The ICP loop for params->max_iters iterations with no host round-trip:
    every iteration is enqueued up front; the pose and the stop flag live in device memory,
    so iterations after convergence, degeneracy or zero correspondences do no work.
+   Correspondences use the certified warm start of SURVEY.md 8(a) row a2 in leaf form: a
+   source point whose previous exact match j1 was found at anchor pose T_a, where every target
+   outside j1's leaf L1 was at distance >= d_out, satisfies G = d_out - d1 > 2 |T p - T_a p|
+   keeps L1 without a search (the nearest neighbour then provably lies in L1: for t not in
+   L1, |s' - t| >= d_out - D > d1 + D >= |s' - t_j1|) and only L1's points are evaluated;
+   every other point gets a full exact search (bounded by 1.1 max_corr_dist).  The result is
+   identical to a full search every iteration up to exact d^2 ties.
    pose_init fp64[16] device; res: device cil_icp_result; iter_log (nullable) device
    fp64[max_iters*2] = {n_corr, rmse} per executed iteration (unexecuted rows are 0). */
 cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
@@ -199,9 +206,26 @@ uint64_t cil_launch_count(void);
 typedef struct {
     double build_ms, nn_ms, acc_ms, query_ms;   /* summed event durations */
     int64_t n_build, n_nn, n_acc, n_query;       /* number of timed launches */
+    double sel_ms;                               /* certificate/selection kernel (cil_icp_run) */
+    int64_t n_sel;
 } cil_profile_stats;
 cil_status cil_profile_enable(int on);
 cil_status cil_profile_read(cil_profile_stats* out);
+
+/* Diagnostics: bit 0 set = cil_icp_run does a full search every iteration (no certified
+   warm start); used to measure the certificate.  Host-only, process-wide. */
+cil_status cil_debug_set_flags(uint32_t flags);
+
+/* Tuning: margin g of the leaf certificate of cil_icp_run as a fraction of max_corr_dist
+   (default 0.002): K_nn searches to (sqrt(best) + g)^2 so that a match is certified to stay
+   in its leaf while the point moves less than about g/2.  0 <= frac <= 1.  Host-only. */
+cil_status cil_debug_set_cert_gap(double frac);
+
+/* Diagnostics: while buf (device int32, >= 16 per query slot) is non-NULL, every search-engine
+   launch writes per processed query slot {flags, r, i0, i1, nF, best d2 after the packet
+   phases, work items, final best d2, SM clocks of phases A, B, C, D+E, F, 0, 0, 0}.  NULL
+   switches it off.  Host-only, process-wide. */
+cil_status cil_debug_engine_trace(int32_t* buf);
 
 #ifdef __cplusplus
 }

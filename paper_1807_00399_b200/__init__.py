@@ -43,7 +43,8 @@ METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_
 
 EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
-            "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read"]
+            "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
+            "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_gap"]
 
 
 class cil_index_params(C.Structure):
@@ -68,7 +69,8 @@ class cil_icp_system(C.Structure):
 
 class cil_profile_stats(C.Structure):
     _fields_ = [("build_ms", C.c_double), ("nn_ms", C.c_double), ("acc_ms", C.c_double), ("query_ms", C.c_double),
-                ("n_build", C.c_int64), ("n_nn", C.c_int64), ("n_acc", C.c_int64), ("n_query", C.c_int64)]
+                ("n_build", C.c_int64), ("n_nn", C.c_int64), ("n_acc", C.c_int64), ("n_query", C.c_int64),
+                ("sel_ms", C.c_double), ("n_sel", C.c_int64)]
 
 
 class cil_target_info(C.Structure):
@@ -102,6 +104,30 @@ _lib.cil_profile_enable.restype = C.c_int
 _lib.cil_profile_enable.argtypes = [C.c_int]
 _lib.cil_profile_read.restype = C.c_int
 _lib.cil_profile_read.argtypes = [C.POINTER(cil_profile_stats)]
+_lib.cil_debug_set_flags.restype = C.c_int
+_lib.cil_debug_set_flags.argtypes = [C.c_uint32]
+_lib.cil_debug_engine_trace.restype = C.c_int
+_lib.cil_debug_engine_trace.argtypes = [C.c_void_p]
+_lib.cil_debug_set_cert_gap.restype = C.c_int
+_lib.cil_debug_set_cert_gap.argtypes = [C.c_double]
+
+# Byte offsets into the ICP workspace (csrc/icp.cu ws_layout, IcpState) -- diagnostics only.
+WS_STATE_SEARCHED = 176       # int64: sum over executed iterations of the search-list size
+
+
+def set_certificates(on: bool = True) -> None:
+    """cil_icp_run: certified warm start on (default) or a full search every iteration (diagnostics)."""
+    _check(_lib.cil_debug_set_flags(0 if on else 1), "cil_debug_set_flags")
+
+
+def set_cert_gap(frac: float) -> None:
+    """leaf-certificate margin g / max_corr_dist of cil_icp_run (tuning; default 0.01)"""
+    _check(_lib.cil_debug_set_cert_gap(float(frac)), "cil_debug_set_cert_gap")
+
+
+def run_searched(ws: torch.Tensor) -> int:
+    """number of full searches cil_icp_run did (sum over iterations), read from the workspace"""
+    return int(ws[WS_STATE_SEARCHED:WS_STATE_SEARCHED + 8].cpu().view(torch.int64).item())
 
 
 def profile_enable(on: bool = True) -> None:

@@ -16,6 +16,20 @@ std::atomic<unsigned long long> g_launches{0};
 void count_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
 
 namespace {
+unsigned g_debug_flags = 0;
+}
+unsigned debug_flags() { return g_debug_flags; }
+namespace {
+int* g_trace = nullptr;
+}
+int* debug_trace() { return g_trace; }
+namespace {
+double g_cert_gap = 0.002;
+}
+double cert_gap_frac() { return g_cert_gap; }
+void set_debug_trace(int* p) { g_trace = p; }
+
+namespace {
 struct ProfRec { int cls; cudaEvent_t a, b; };
 bool g_prof = false;
 std::vector<cudaEvent_t> g_pool;
@@ -121,6 +135,7 @@ CIL_API cil_status cil_profile_read(cil_profile_stats* out) {
             case cil::kProfBuild: out->build_ms += ms; ++out->n_build; break;
             case cil::kProfNN: out->nn_ms += ms; ++out->n_nn; break;
             case cil::kProfAcc: out->acc_ms += ms; ++out->n_acc; break;
+            case cil::kProfSel: out->sel_ms += ms; ++out->n_sel; break;
             default: out->query_ms += ms; ++out->n_query; break;
         }
         cil::g_pool.push_back(r.a);
@@ -130,6 +145,17 @@ CIL_API cil_status cil_profile_read(cil_profile_stats* out) {
     return CIL_OK;
 }
 
+CIL_API cil_status cil_debug_set_cert_gap(double frac) {
+    if (!(frac >= 0.0) || frac > 1.0) return CIL_ERR_INVALID_ARG;
+    cil::g_cert_gap = frac;
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_debug_set_flags(uint32_t flags) {
+    cil::g_debug_flags = flags;
+    return CIL_OK;
+}
+
 CIL_API uint64_t cil_launch_count(void) { return (uint64_t)cil::g_launches.load(); }
 
-CIL_API const char* cil_version(void) { return "cil-b200 0.1 (sm_100a)"; }
+CIL_API const char* cil_version(void) { return "cil-b200 0.2 (sm_100a)"; }

@@ -4,20 +4,28 @@
 // on-device 6x6 Cholesky solve and pose update, so an iteration loop launches with no host
 // round-trip".
 //
-// One iteration = two launches:
-//   K_nn  (correspondence kernel, north_star subsystem (3)): persistent search engine
-//         (search.cuh) -- a1 s = R p_i + t (fp64 -> double-float), a2 exact 1-NN bounded by
-//         max_corr_dist (a3: nothing within the bound = rejected), hint leaf = the previous
-//         iteration's match in cil_icp_run; writes nn_pos[i] (sorted target position or -1).
+// One iteration of cil_icp_run = three launches:
+//   K_sel (certified warm start): for every source point, its previous
+//         exact match j1 found at anchor pose T_a with 2nd-best gap G = d2 - d1 stays exact
+//         at the current pose T if G > 2 |(R - R_a) p + (t - t_a)| (with rounding margins);
+//         every other point is appended to the search list.
+//   K_nn  (correspondence kernel, north_star subsystem (3)): persistent warp-packet search
+//         engine (search.cuh) over the list -- a1 s = R p_i + t (fp64 -> double-float), a2
+//         exact 1-NN and exact 2nd-best d2 bounded by rho = 1.1 max_corr_dist, hint leaf =
+//         the previous match; writes nn[i] (original target index or -1) and the gap word
+//         (gap rounded toward zero, low 8 bits = anchor slot).
 //   K_acc (fused transform+reject+J^TJ/J^Tr kernel, subsystem (4)), static grid-stride:
-//     a1  s = R p_i + t again (fp64 -> double-float)
+//     a1  s = R p_i + t again (fp64 -> double-float), d2 to t_nn[i] (same arithmetic as K_nn)
+//     a3  accept iff d2 <= fl32(max_corr_dist^2)
 //     a4  residual + Jacobian of the metric for accepted pairs (PAPER.md:140 [Besl], [Low])
 //     a5  fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
 //   warp: transposed butterfly reduce (31 SHFL for 32 values; lane k ends with sum k)
 //   block: per-warp fp64 sums -> per-CTA fp64 partial in the workspace
 //   last CTA (ticket): ordered fp64 sum of the partials -> a6 Cholesky solve -> a7 pose update,
-//   status, log.  Results are bitwise reproducible run to run (fixed grid, fixed orders,
-//   no floating-point atomics).
+//   status, log, anchor-pose table for the next K_sel.  Results are bitwise reproducible run
+//   to run (fixed grid, fixed orders, no floating-point atomics; the search result of a
+//   query does not depend on which warp searches it).
+// cil_icp_iterate = K_nn over all points (no hints, bound max_corr_dist) + K_acc.
 #include "internal.cuh"
 #include "search.cuh"
 
@@ -34,7 +42,10 @@ struct IterArgs {
     TargetView T;
     const float* src;
     int m;
-    float bound2;
+    float bound2;            // fl32(max_corr_dist^2): acceptance (a3)
+    float search2;           // search bound: bound2, or fl32(rho^2) with certificates
+    float gap_none;          // certificate of "no target within rho": rho - max_corr_dist (rounded down)
+    float cert_gap;          // search-threshold margin g of the leaf certificate
     const double* pose_in;
     double* pose_out;
     double* partials;        // [kMaxCtas * kSlots]
@@ -42,10 +53,15 @@ struct IterArgs {
     cil_icp_system* sys;     // iterate only, nullable
     int32_t* corr_idx;       // iterate only, nullable
     float* corr_d2;          // iterate only, nullable
-    int* nn_pos;             // [m] match per query (sorted target position or -1), written by K_nn
-    int warm;                // K_nn: use nn_pos as the hint (cil_icp_run after its first iteration)
+    int* nn;                 // [m] match per query (original target index or -1)
+    uint32_t* gw;            // [m] gap word (run): bits(gap) & ~255 | anchor slot
+    int* list;               // [m] uncertified queries of this iteration (run with certificates)
+    unsigned long long* sel_status;   // [tiles] chained-scan status of K_sel (run)
+    double* apose;           // [kAnchorSlots][12] pose of each anchor slot (run)
+    float* adelta;           // [kAnchorSlots][16] (R - R_a | t - t_a | max|dR| | max|dt|) for the current pose
     double* iter_log;        // run only, nullable
     int run;
+    int cert;                // run: certified warm start on
     double rot_tol, trans_tol;
 };
 
@@ -65,7 +81,7 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[kSlots]) {
 }
 
 // ---------------------------------------------------------------- a6 + a7 (one thread)
-__device__ void rodrigues(const double a[3], double R[9]) {
+__device__ __noinline__ void rodrigues(const double a[3], double R[9]) {
     const double th2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
     const double th = sqrt(th2);
     double A, Bc;
@@ -85,7 +101,7 @@ __device__ void rodrigues(const double a[3], double R[9]) {
 
 // Build (H, g, sse, count) from the reduced sums of the metric.
 template <int METRIC>
-__device__ void assemble(const double* S, double H[36], double g[6], double& sse, double& cnt) {
+__device__ __noinline__ void assemble(const double* S, double H[36], double g[6], double& sse, double& cnt) {
     if (METRIC == CIL_POINT_TO_PLANE) {
         int k = 0;
         for (int a = 0; a < 6; ++a)
@@ -116,7 +132,7 @@ __device__ void assemble(const double* S, double H[36], double g[6], double& sse
 }
 
 // Cholesky solve of H x = -g with the degeneracy rule of DESIGN.md R9; returns status.
-__device__ int solve6(const double H[36], const double g[6], double cnt, double x[6]) {
+__device__ __noinline__ int solve6(const double H[36], const double g[6], double cnt, double x[6]) {
     for (int i = 0; i < 6; ++i) x[i] = 0.0;
     if (cnt == 0.0) return CIL_NO_CORRESPONDENCES;
     if (cnt < 6.0) return CIL_ERR_DEGENERATE;
@@ -153,7 +169,7 @@ __device__ int solve6(const double H[36], const double g[6], double cnt, double 
 }
 
 template <int METRIC>
-__device__ void finalize(const IterArgs& a, const double* S, const double* P) {
+__device__ __noinline__ void finalize(const IterArgs& a, const double* S, const double* P) {
     double H[36], g[6], x[6], sse, cnt;
     assemble<METRIC>(S, H, g, sse, cnt);
     const int status = solve6(H, g, cnt, x);
@@ -200,51 +216,165 @@ __device__ void finalize(const IterArgs& a, const double* S, const double* P) {
     }
 }
 
+// ---------------------------------------------------------------- K_sel (certified warm start)
+// Displacement bound of source point p between its anchor pose T_a and the current pose T:
+// v = (R - R_a) p + (t - t_a) in fp32 from the per-slot table; the bound adds the rounding
+// of the table entries and of the 3-term dot products (|err_k| <= 2^-21 (max|dR| |p|_1 +
+// max|dt|)), and an absolute 2^-30 (|p|_1 + 1) for the double-float representation of s.
+__device__ __forceinline__ float displacement_bound(const float* __restrict__ D, float px, float py, float pz) {
+    const float4 d0 = __ldg(reinterpret_cast<const float4*>(D));
+    const float4 d1 = __ldg(reinterpret_cast<const float4*>(D) + 1);
+    const float4 d2 = __ldg(reinterpret_cast<const float4*>(D) + 2);
+    const float4 d3 = __ldg(reinterpret_cast<const float4*>(D) + 3);
+    // D = [dR00 dR01 dR02 dR10 | dR11 dR12 dR20 dR21 | dR22 dt0 dt1 dt2 | M T 0 0]
+    const float vx = fmaf(d0.x, px, fmaf(d0.y, py, fmaf(d0.z, pz, d2.y)));
+    const float vy = fmaf(d0.w, px, fmaf(d1.x, py, fmaf(d1.y, pz, d2.z)));
+    const float vz = fmaf(d1.z, px, fmaf(d1.w, py, fmaf(d2.x, pz, d2.w)));
+    const float p1 = fabsf(px) + fabsf(py) + fabsf(pz);
+    const float nv = sqrtf(fmaf(vx, vx, fmaf(vy, vy, vz * vz)));
+    return fmaf(nv, 1.0f + 0x1p-20f, fmaf(0x1p-19f, fmaf(d3.x, p1, d3.y), 0x1p-30f * (p1 + 1.0f)));
+}
+
+// Order-preserving compaction (the list keeps source order, so a 32-query packet of the
+// search stays spatially coherent): one tile of kSelTile consecutive queries per CTA, tile
+// ids from a ticket (so every lower tile is already running), single-pass chained scan
+// with decoupled look-back over per-tile status words (epoch | flag | count) in one u64.
+constexpr int kSelThreads = 256;
+constexpr int kSelRounds = 8;
+constexpr int kSelTile = kSelThreads * kSelRounds;     // 2048 queries per tile
+
+__device__ __forceinline__ bool needs_search(const IterArgs& a, int i, uint32_t kslot) {
+    const uint32_t w = a.gw[i];
+    const float G = __uint_as_float(w & ~255u);
+    const uint32_t slot = w & 255u;
+    // slot == kslot only after 256 iterations: that anchor pose is being recycled
+    if (!(G > 0.0f) || slot == kslot) return true;
+    const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
+    const float D = displacement_bound(a.adelta + 16 * slot, px, py, pz);
+    return a.nn[i] >= 0 ? !(G > 2.0f * D) : !(G > D);
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+icp_select_kernel(const IterArgs a) {
+    __shared__ int s_tile, s_base;
+    __shared__ int s_wsum[kSelThreads / 32];
+    if (*(volatile int*)&a.st->done) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int k = *(volatile int*)&a.st->iters;
+    const uint32_t kslot = (uint32_t)k & (kAnchorSlots - 1);
+    const unsigned long long epoch = (unsigned long long)((k + 1) & 0xffff);
+    if (threadIdx.x == 0) s_tile = atomicAdd(&a.st->sel_ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int wbase = tile * kSelTile + warp * (32 * kSelRounds);
+    unsigned masks[kSelRounds];
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < kSelRounds; ++r) {
+        const int i = wbase + 32 * r + lane;
+        masks[r] = __ballot_sync(FULL, i < a.m && needs_search(a, i, kslot));
+        cnt += __popc(masks[r]);
+    }
+    if (lane == 0) s_wsum[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) { const int c = s_wsum[w]; s_wsum[w] = tot; tot += c; }
+        unsigned long long* stat = a.sel_status;
+        int excl = 0;
+        if (tile > 0) {
+            atomicExch(stat + tile, (epoch << 48) | (1ull << 32) | (unsigned)tot);
+            for (int p = tile - 1; p >= 0;) {
+                const unsigned long long v = *(volatile unsigned long long*)(stat + p);
+                if ((v >> 48) != epoch) continue;                       // predecessor not published yet
+                excl += (int)(v & 0xffffffffull);
+                if (((v >> 32) & 3ull) == 2ull) break;                  // inclusive prefix: done
+                --p;
+            }
+        }
+        atomicExch(stat + tile, (epoch << 48) | (2ull << 32) | (unsigned)(excl + tot));
+        if (tile == (int)gridDim.x - 1) a.st->list_n = excl + tot;
+        s_base = excl;
+    }
+    __syncthreads();
+    int pos = s_base + s_wsum[warp];
+#pragma unroll
+    for (int r = 0; r < kSelRounds; ++r) {
+        if ((masks[r] >> lane) & 1u) a.list[pos + __popc(masks[r] & lt)] = wbase + 32 * r + lane;
+        pos += __popc(masks[r]);
+    }
+}
+
 // ---------------------------------------------------------------- K_nn
 constexpr int kNNThreads = 256;
 
-template <int B>
+template <int B, bool CERT>
 struct IcpQueries {
     const float* src;
+    const float4* opts;
     Pose34 P;
-    float bound2;
-    int* nn_pos;
+    float search2;
+    float gap_none;
+    float gap;               // CERT: search-threshold margin g (leaf form)
+    int* nn;
+    uint32_t* gw;
+    const int* list;
     int warm;
+    uint32_t slot;
     int32_t* corr_idx;
     float* corr_d2;
-    __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
+    __device__ __forceinline__ bool load(int k, DF3& s, unsigned long long& init, int& hint) const {
+        const int i = list ? list[k] : k;
         s = transform_df(P, src[3 * (size_t)i], src[3 * (size_t)i + 1], src[3 * (size_t)i + 2]);
-        init = bound_key(bound2);
-        const int jp = warm ? nn_pos[i] : -1;
-        hint = jp >= 0 ? jp / B : -1;
+        init = bound_key(search2);
+        const int j = warm ? nn[i] : -1;
+        hint = j >= 0 ? __float_as_int(__ldg(&opts[j].w)) / B : -1;
         return true;
     }
-    __device__ __forceinline__ void store(int i, unsigned long long best, int bpos, const DF3&) const {
-        const bool found = best != bound_key(bound2);
-        nn_pos[i] = found ? bpos : -1;
+    __device__ __forceinline__ void store(int k, unsigned long long best, float lb_out2) const {
+        const int i = list ? list[k] : k;
+        const bool found = best != bound_key(search2);
+        nn[i] = found ? (int)key_idx(best) : -1;
+        if (CERT) {
+            // leaf certificate G = d_out - d1: every target outside the winner's leaf is at
+            // fp32 distance >= sqrt(lb_out2); 4e-6 relative slack covers the fp32 d^2 error,
+            // rounded toward zero by clearing the low 8 bits (they hold the anchor slot)
+            float G = gap_none;
+            if (found) G = fmaxf(sqrtf(lb_out2) * (1.0f - 4e-6f) - sqrtf(key_d2(best)) * (1.0f + 4e-6f), 0.0f);
+            gw[i] = (__float_as_uint(G) & ~255u) | slot;
+        }
         if (corr_idx) corr_idx[i] = found ? (int32_t)key_idx(best) : -1;
         if (corr_d2) corr_d2[i] = found ? key_d2(best) : INFINITY;
     }
 };
 
-template <int B>
+template <int B, bool CERT>
 __global__ void __launch_bounds__(kNNThreads)
 icp_nn_kernel(const IterArgs a) {
     if (a.run && *(volatile int*)&a.st->done) return;
-    IcpQueries<B> qs;
+    IcpQueries<B, CERT> qs;
     qs.src = a.src;
+    qs.opts = a.T.opts;
 #pragma unroll
     for (int k = 0; k < 12; ++k) qs.P.r[k] = __ldg(a.pose_in + k);
-    qs.bound2 = a.bound2;
-    qs.nn_pos = a.nn_pos;
-    qs.warm = a.warm;
+    qs.search2 = a.search2;
+    qs.gap_none = a.gap_none;
+    qs.gap = a.cert_gap;
+    qs.nn = a.nn;
+    qs.gw = a.gw;
+    qs.list = a.cert ? a.list : nullptr;
+    qs.warm = a.run;
+    qs.slot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     qs.corr_idx = a.corr_idx;
     qs.corr_d2 = a.corr_d2;
-    nn_packet_engine<B>(a.T, qs, a.m, &a.st->work);
+    const int m = a.cert ? *(volatile int*)&a.st->list_n : a.m;
+    nn_packet_engine<B, CERT>(a.T, qs, m, &a.st->work);
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
-template <int METRIC>
+template <int METRIC, int B>
 __global__ void __launch_bounds__(kIcpThreads)
 icp_acc_kernel(const IterArgs a) {
     __shared__ double wsum[kIcpWarps][kSlots];
@@ -265,17 +395,29 @@ icp_acc_kernel(const IterArgs a) {
 
     const TargetView& T = a.T;
     const int stride = gridDim.x * blockDim.x;
+    const uint32_t kslot = a.cert ? ((uint32_t)a.st->iters & (kAnchorSlots - 1)) : 0u;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += stride) {
-        const int bpos = a.nn_pos[i];
-        if (bpos < 0) continue;                                         // a3: rejected
+        int j = a.nn[i];
+        if (j < 0) continue;                                            // a3: nothing within the bound
         const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1],
                                    a.src[3 * (size_t)i + 2]);            // a1
-        const float4 t = __ldg(T.pts + bpos);
+        float4 t = __ldg(T.opts + j);
+        if (a.cert && (a.gw[i] & 255u) != kslot) {
+            // certified (K_sel): the exact nearest neighbour lies in the previous match's leaf
+            const int leaf = __float_as_int(t.w) / B;
+            const NegQuery nq = neg_query(s);
+            float d2[B];
+            leaf_d2<B>(T, nq, leaf, d2);
+            const float m1 = leaf_min<B>(d2);
+            const int jn = (int)leaf_argmin<B>(T, leaf, d2, m1);
+            if (jn != j) { a.nn[i] = jn; j = jn; t = __ldg(T.opts + j); }
+        }
         const float dx = dfdiff(s.hx, s.lx, t.x);
         const float dy = dfdiff(s.hy, s.ly, t.y);
         const float dz = dfdiff(s.hz, s.lz, t.z);
+        if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= a.bound2)) continue;   // a3 (inclusive, R2)
         if (METRIC == CIL_POINT_TO_PLANE) {                             // a4 + a5
-            const float4 n = __ldg(T.nrm + bpos);
+            const float4 n = __ldg(T.onrm + j);
             const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
             const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
                                 fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
@@ -334,24 +476,56 @@ icp_acc_kernel(const IterArgs a) {
         for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
         Ssum[threadIdx.x] = v;
     }
+    const int it = a.run ? a.st->iters : 0;                 // index of this iteration
+    if (a.cert && threadIdx.x < 12) a.apose[12 * (it & (kAnchorSlots - 1)) + threadIdx.x] = Psh[threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {
         finalize<METRIC>(a, Ssum, Psh);
         a.st->ticket = 0;
         a.st->work = 0;      // K_nn's counter, for the next iteration
+        a.st->searched += a.run ? a.st->list_n : 0;
+        a.st->list_n = 0;
+        a.st->sel_ticket = 0;
+    }
+    __syncthreads();
+    // anchor table for the next iteration's K_sel: delta of every live slot to the new pose
+    if (a.cert && !a.st->done) {
+        const int a_slot = threadIdx.x;
+        if (a_slot < kAnchorSlots && a_slot <= it) {
+            const double* Pa = a.apose + 12 * a_slot;
+            const volatile double* Pn = a.st->pose;
+            float* D = a.adelta + 16 * a_slot;
+            double M = 0.0, Tm = 0.0;
+            const int rot[9] = {0, 1, 2, 4, 5, 6, 8, 9, 10};
+            for (int e = 0; e < 9; ++e) {
+                const double d = Pn[rot[e]] - Pa[rot[e]];
+                D[e] = (float)d;
+                M = fmax(M, fabs(d));
+            }
+            for (int e = 0; e < 3; ++e) {
+                const double d = Pn[4 * e + 3] - Pa[4 * e + 3];
+                D[9 + e] = (float)d;
+                Tm = fmax(Tm, fabs(d));
+            }
+            D[12] = __double2float_ru(M);
+            D[13] = __double2float_ru(Tm);
+            D[14] = 0.0f;
+            D[15] = 0.0f;
+        }
     }
 }
 
 // ---------------------------------------------------------------- run bookkeeping kernels
-__global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn_prev, int m,
-                                double* iter_log, int log_len) {
+__global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, uint32_t* gw, int m,
+                                unsigned long long* sel_status, double* iter_log, int log_len) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0) {
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
-        st->done = 0; st->ticket = 0; st->work = 0;
+        st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->sel_ticket = 0;
     }
-    for (int i = tid; i < m; i += gridDim.x * blockDim.x) nn_prev[i] = -1;
+    for (int i = tid; i < (m + kSelTile - 1) / kSelTile; i += gridDim.x * blockDim.x) sel_status[i] = 0ull;
+    for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; }
     if (iter_log)
         for (int i = tid; i < log_len; i += gridDim.x * blockDim.x) iter_log[i] = 0.0;
 }
@@ -367,7 +541,7 @@ __global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
     res->pad = 0;
 }
 
-__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; }
+__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; }
 
 template <class K>
 int occupancy_of(K kernel, int threads) {
@@ -382,52 +556,96 @@ inline int persistent_grid(int occ, int threads, int m, int cap_ctas) {
     return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
-template <int B>
+template <int B, bool CERT>
 cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
-    static const int occ = occupancy_of(icp_nn_kernel<B>, kNNThreads);
+    static const int occ = occupancy_of(icp_nn_kernel<B, CERT>, kNNThreads);
     const int g = persistent_grid(occ, kNNThreads, a.m, 1 << 20);
     prof_begin(kProfNN, s);
-    icp_nn_kernel<B><<<g, kNNThreads, 0, s>>>(a);
+    IterArgs ad = a;
+    ad.T.trace = debug_trace();
+    ad.T.dbg_mode = (int)(debug_flags() >> 1) & 3;
+    icp_nn_kernel<B, CERT><<<g, kNNThreads, 0, s>>>(ad);
+    prof_end(s);
+    return cudaGetLastError();
+}
+
+template <bool CERT>
+cudaError_t launch_nn_t(const IterArgs& a, cudaStream_t s) {
+    switch (a.T.leaf_size) {
+        case 4: return launch_nn_b<4, CERT>(a, s);
+        case 8: return launch_nn_b<8, CERT>(a, s);
+        case 16: return launch_nn_b<16, CERT>(a, s);
+        default: return launch_nn_b<32, CERT>(a, s);
+    }
+}
+
+template <int METRIC, int B>
+cudaError_t launch_acc_mb(const IterArgs& a, cudaStream_t s) {
+    static const int occ = occupancy_of(icp_acc_kernel<METRIC, B>, kIcpThreads);
+    const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
+    prof_begin(kProfAcc, s);
+    icp_acc_kernel<METRIC, B><<<g, kIcpThreads, 0, s>>>(a);
     prof_end(s);
     return cudaGetLastError();
 }
 
 template <int METRIC>
 cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
-    static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads);
-    const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
-    prof_begin(kProfAcc, s);
-    icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
-    prof_end(s);
-    return cudaGetLastError();
+    switch (a.T.leaf_size) {
+        case 4: return launch_acc_mb<METRIC, 4>(a, s);
+        case 8: return launch_acc_mb<METRIC, 8>(a, s);
+        case 16: return launch_acc_mb<METRIC, 16>(a, s);
+        default: return launch_acc_mb<METRIC, 32>(a, s);
+    }
 }
 
-// one ICP iteration = K_nn + K_acc
+// one ICP iteration = [K_sel] + K_nn + K_acc
 cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
-    count_launches(2);
-    cudaError_t e;
-    switch (a.T.leaf_size) {
-        case 4: e = launch_nn_b<4>(a, s); break;
-        case 8: e = launch_nn_b<8>(a, s); break;
-        case 16: e = launch_nn_b<16>(a, s); break;
-        default: e = launch_nn_b<32>(a, s); break;
+    int n = 2;
+    if (a.cert) {
+        const int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
+        prof_begin(kProfSel, s);
+        icp_select_kernel<<<g, kSelThreads, 0, s>>>(a);
+        prof_end(s);
+        ++n;
     }
+    count_launches(n);
+    cudaError_t e = a.cert ? launch_nn_t<true>(a, s) : launch_nn_t<false>(a, s);
     if (e != cudaSuccess) return e;
     return metric == CIL_POINT_TO_PLANE ? launch_acc_m<CIL_POINT_TO_PLANE>(a, s)
                                         : launch_acc_m<CIL_POINT_TO_POINT>(a, s);
 }
 
 struct WsLayout {
-    size_t state, partials, nn_prev, total;
+    size_t state, partials, apose, adelta, nn, gw, list, sel, total;
 };
 
 WsLayout ws_layout(int64_t m) {
+    const size_t mm = (size_t)std::max<int64_t>(m, 1);
     WsLayout L;
     L.state = 0;
     L.partials = 256;
-    L.nn_prev = L.partials + align_up((size_t)kMaxCtas * kSlots * sizeof(double), 256);
-    L.total = L.nn_prev + align_up((size_t)std::max<int64_t>(m, 1) * sizeof(int), 256);
+    L.apose = L.partials + align_up((size_t)kMaxCtas * kSlots * sizeof(double), 256);
+    L.adelta = L.apose + align_up((size_t)kAnchorSlots * 12 * sizeof(double), 256);
+    L.nn = L.adelta + align_up((size_t)kAnchorSlots * 16 * sizeof(float), 256);
+    L.gw = L.nn + align_up(mm * sizeof(int), 256);
+    L.list = L.gw + align_up(mm * sizeof(uint32_t), 256);
+    L.sel = L.list + align_up(mm * sizeof(int), 256);
+    L.total = L.sel + align_up((mm + kSelTile - 1) / kSelTile * sizeof(unsigned long long), 256);
     return L;
+}
+
+void bind_ws(IterArgs& a, void* ws, int64_t m) {
+    const WsLayout L = ws_layout(m);
+    char* w = (char*)ws;
+    a.st = (IcpState*)(w + L.state);
+    a.partials = (double*)(w + L.partials);
+    a.apose = (double*)(w + L.apose);
+    a.adelta = (float*)(w + L.adelta);
+    a.nn = (int*)(w + L.nn);
+    a.gw = (uint32_t*)(w + L.gw);
+    a.list = (int*)(w + L.list);
+    a.sel_status = (unsigned long long*)(w + L.sel);
 }
 
 cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
@@ -475,24 +693,20 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     cil_status rc = check_common("cil_icp_iterate", t, src, m, params, ws, ws_bytes);
     if (rc != CIL_OK) return rc;
     if (!pose_in || !pose_out) { set_error("cil_icp_iterate: pose_in/pose_out NULL"); return CIL_ERR_INVALID_ARG; }
-    const WsLayout L = ws_layout(m);
-    char* w = (char*)ws;
     IterArgs a{};
+    bind_ws(a, ws, m);
     a.T = t->v;
     a.src = src;
     a.m = (int)m;
     a.bound2 = bound2_of(params->max_corr_dist);
+    a.search2 = a.bound2;
     a.pose_in = pose_in;
     a.pose_out = pose_out;
-    a.partials = (double*)(w + L.partials);
-    a.st = (IcpState*)(w + L.state);
     a.sys = sys;
     a.corr_idx = corr_idx;
     a.corr_d2 = corr_sqdist;
-    a.nn_pos = (int*)(w + L.nn_prev);
-    a.warm = 0;
-    a.iter_log = nullptr;
     a.run = 0;
+    a.cert = 0;
     cudaStream_t s = (cudaStream_t)stream;
     reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
     count_launches(1);
@@ -508,31 +722,39 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     if (rc != CIL_OK) return rc;
     if (!pose_init || !res) { set_error("cil_icp_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
     if (params->max_iters < 1) { set_error("cil_icp_run: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
-    const WsLayout L = ws_layout(m);
-    char* w = (char*)ws;
     IterArgs a{};
+    bind_ws(a, ws, m);
     a.T = t->v;
     a.src = src;
     a.m = (int)m;
     a.bound2 = bound2_of(params->max_corr_dist);
-    a.st = (IcpState*)(w + L.state);
+    a.cert = (debug_flags() & 1u) ? 0 : 1;
+    // certificates search to rho = 1.1 max_corr_dist so that a point with
+    // nothing within rho stays provably rejected while it moves less than rho - max_corr_dist
+    const double rho = std::isinf(params->max_corr_dist) ? INFINITY : 1.1 * params->max_corr_dist;
+    a.search2 = a.cert ? bound2_of(rho) : a.bound2;
+    {
+        const double gn = (rho - params->max_corr_dist) * (1.0 - 1e-6);
+        float g = std::isfinite(gn) ? (float)gn : 0.0f;
+        if ((double)g > gn) g = std::nextafter(g, 0.0f);
+        a.gap_none = g;
+    }
+    // leaf-certificate margin g: the search threshold of K_nn is (sqrt(best) + g)^2
+    a.cert_gap = (float)(cert_gap_frac() * (std::isinf(params->max_corr_dist) ? 0.0 : params->max_corr_dist));
     a.pose_in = a.st->pose;
     a.pose_out = a.st->pose;
-    a.partials = (double*)(w + L.partials);
-    a.nn_pos = (int*)(w + L.nn_prev);
-    a.warm = 0;
     a.iter_log = iter_log;
     a.run = 1;
     a.rot_tol = params->rot_tol;
     a.trans_tol = params->trans_tol;
     cudaStream_t s = (cudaStream_t)stream;
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
-    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn_pos, (int)m, iter_log, 2 * params->max_iters);
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, (int)m, a.sel_status, iter_log,
+                                                2 * params->max_iters);
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
     for (int it = 0; it < params->max_iters; ++it) {
-        a.warm = it > 0;
         e = launch_iter(a, params->metric, s);
         if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
     }

@@ -21,10 +21,11 @@ constexpr int kMortonBits = 16;
 
 // The target, as the kernels see it (device pointers + sizes).  Passed by value.
 struct TargetView {
-    const float4* pts;    // [n] sorted by Morton key: x, y, z, __int_as_float(original index)
-    const float4* nrm;    // [n] normals in the same order (w unused) or nullptr
+    const float4* opts;   // [n] ORIGINAL order: x, y, z, __int_as_float(sorted position)
+    const float4* onrm;   // [n] ORIGINAL order normals (w unused) or nullptr
     const float4* box;    // [2 * 2 * l_pad]: node v (1-based heap) -> box[2v] = lo, box[2v+1] = hi
     const float4* leafsoa;  // [n_leaves * B]: per leaf rows x[B], y[B], z[B], idx[B] (padding: +inf, idx ~0)
+    const float4* lbox;   // [2 * n_leaves]: leaf boxes interleaved (lo.x, hi.x, lo.y, hi.y), (lo.z, hi.z, 0, 0)
     const unsigned long long* keys;  // [n] sorted 48-bit Morton keys of pts
     const uint32_t* cell_first;      // [2^coarse_bits + 1]: first sorted index with key >> (48-coarse_bits) >= c
     const float4* quant;  // [1]: (min.x, min.y, min.z, cells per unit) of the Morton quantisation
@@ -33,6 +34,8 @@ struct TargetView {
     int levels;           // log2(l_pad)
     int leaf_size;
     int coarse_bits;      // multiple of 3, <= 21
+    int* trace;           // diagnostics only (cil_debug_engine_trace), normally nullptr
+    int dbg_mode;         // diagnostics only (cil_debug_set_flags bits 1-2), normally 0
 };
 
 struct cil_target {
@@ -44,19 +47,24 @@ struct cil_target {
     size_t bytes;
 };
 
-// Device-resident ICP state at the head of the workspace.
+// Device-resident ICP state at the head of the workspace (offsets are read by tools/).
 struct alignas(256) IcpState {
-    double pose[16];
-    double rmse;
-    long long n_corr;
-    int iters;
-    int converged;
-    int status;
-    int done;
-    unsigned int ticket;
-    unsigned int work;    // dynamic work counter of the correspondence kernel
-    int pad_[2];
+    double pose[16];      // 0
+    double rmse;          // 128
+    long long n_corr;     // 136
+    int iters;            // 144: iterations executed so far (= index of the running one)
+    int converged;        // 148
+    int status;           // 152
+    int done;             // 156
+    unsigned int ticket;  // 160: last-CTA ticket of the accumulation kernel
+    unsigned int work;    // 164: dynamic work counter of the search kernel
+    int list_n;           // 168: uncertified queries of the running iteration (search list size)
+    int sel_ticket;       // 172: tile ticket of the selection kernel
+    long long searched;   // 176: sum over executed iterations of list_n (diagnostics)
 };
+
+// Certified warm start: anchor-pose ring of cil_icp_run.
+constexpr int kAnchorSlots = 256;   // anchor id = iteration & 255 (low 8 bits of the gap word)
 
 namespace cil {
 
@@ -71,9 +79,13 @@ int sm_count();            // of the current device (cached per device)
 cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s);
 cudaError_t pool_free(void* p, cudaStream_t s);
 void count_launches(int k);   // diagnostics counter behind cil_launch_count()
+unsigned debug_flags();       // cil_debug_set_flags (bit 0: no certified warm start)
+int* debug_trace();           // cil_debug_engine_trace buffer (nullptr = off)
+double cert_gap_frac();       // leaf-certificate margin g / max_corr_dist (cil_debug_set_cert_gap)
+void set_debug_trace(int* p);
 
 // diagnostics: per-launch event timing (cil_profile_*)
-enum ProfClass { kProfBuild = 0, kProfNN = 1, kProfAcc = 2, kProfQuery = 3 };
+enum ProfClass { kProfBuild = 0, kProfNN = 1, kProfAcc = 2, kProfQuery = 3, kProfSel = 4 };
 bool prof_on();
 void prof_begin(int cls, cudaStream_t s);   // records the start event of a timed region
 void prof_end(cudaStream_t s);              // records the end event

@@ -28,7 +28,7 @@ struct NNQueries {
         hint = -1;
         return true;
     }
-    __device__ __forceinline__ void store(int k, unsigned long long best, int, const DF3&) const {
+    __device__ __forceinline__ void store(int k, unsigned long long best, float) const {
         const size_t i = perm[k];
         const bool found = best != bound_key(bound2);
         if (idx) idx[i] = found ? (int32_t)key_idx(best) : -1;
@@ -57,7 +57,7 @@ __global__ void qcell_scatter_kernel(const uint32_t* __restrict__ qcell, int m, 
 template <int B>
 __global__ void __launch_bounds__(kNNThreads)
 nn_query_kernel(TargetView T, NNQueries qs, int m, unsigned int* counter) {
-    nn_packet_engine<B>(T, qs, m, counter);
+    nn_packet_engine<B, false>(T, qs, m, counter);
 }
 
 template <int B>
@@ -70,7 +70,10 @@ cudaError_t launch_nn(const TargetView& T, const NNQueries& qs, int m, unsigned 
     }
     const int64_t want = ((int64_t)m + kNNThreads - 1) / kNNThreads;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ));
-    nn_query_kernel<B><<<blocks, kNNThreads, 0, s>>>(T, qs, m, counter);
+    TargetView Tv = T;
+    Tv.trace = debug_trace();
+    Tv.dbg_mode = (int)(debug_flags() >> 1) & 3;
+    nn_query_kernel<B><<<blocks, kNNThreads, 0, s>>>(Tv, qs, m, counter);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -1,20 +1,10 @@
 // search.cuh -- device side of the exact 1-NN search.
 //
-// Index: target points sorted by 48-bit Morton key, grouped into leaves of B consecutive
-// points, with an implicit complete binary tree of AABBs over the leaves (node v has
-// children 2v, 2v+1; leaves are nodes l_pad .. 2 l_pad - 1).
-//
-// Search ("hint leaf, then ascend"): evaluate a hint leaf (the warm-start match of the
-// previous ICP iteration, or the leaf holding the first target of the query's coarse Morton
-// cell), then walk up the ancestors of that leaf.  At each ancestor u:
-//   * STOP if the ball B(s, sqrt(best)) provably holds no target outside u's subtree:
-//     every target in the ball has a Morton key in [code(ball_lo), code(ball_hi)] (the key is
-//     monotone in each quantised coordinate; one quantum of margin absorbs rounding), and
-//     u's subtree is exactly the sorted key range [key[a], key[b-1]]; so if
-//     key[a-1] < code(ball_lo) and code(ball_hi) < key[b] nothing outside can be in the ball;
-//   * otherwise test u's sibling box and search it (nearest-child-first DFS) if its lower
-//     bound does not exceed the best distance.
-// The subtrees of the siblings of all ancestors partition the tree, so the search is exact.
+// Index (target.cu): target points sorted by 48-bit Morton key, grouped into leaves of B
+// consecutive points (SoA blocks x[B], y[B], z[B], idx[B]), per-leaf boxes in an interleaved
+// layout for the packed lower-bound test, and an implicit complete binary tree of AABBs over
+// the leaves (node v has children 2v, 2v+1; leaves are nodes l_pad .. 2 l_pad - 1).
+// The search itself is the warp-packet engine at the end of this file.
 //
 // Precision contract:
 //  * the transformed query s = R p + t is computed in fp64 and carried as a double-float
@@ -24,10 +14,10 @@
 //  * the minimum is taken over the u64 key (bits(d^2) << 32) | original_index, which orders
 //    by d^2 (non-negative IEEE floats order like their bit patterns) and breaks exact ties
 //    by the lowest original index (R1);
-//  * a box is pruned iff its lower bound lb^2 > best d^2, where lb is computed with the
-//    SAME rounded operations as the candidate differences, so by monotonicity of IEEE
-//    rounding lb^2 <= d^2 of every point inside the box: pruning never drops a point that
-//    could win (or tie) under the kernel's own arithmetic -- the search is exact.
+//  * a box is pruned iff its lower bound lb^2 > the search threshold, where lb is computed
+//    with the SAME rounded operations as the candidate differences, so by monotonicity of
+//    IEEE rounding lb^2 <= d^2 of every point inside the box: pruning never drops a point
+//    that could win (or tie) under the kernel's own arithmetic -- the search is exact.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -128,11 +118,11 @@ __device__ __forceinline__ void offer(const DF3& s, float4 t, int j, unsigned lo
     if (k < best) { best = k; bpos = j; }
 }
 
+
 // ---------------------------------------------------------------- leaf evaluation
-// A leaf is a block of B consecutive sorted targets stored as rows x[B], y[B], z[B], idx[B]
-// (leafsoa).  Two candidates per instruction with the sm_100 packed FP32 ops (FADD2, FFMA2,
-// FMUL2): -dx = (t + (-s_hi)) + (-s_lo) is exactly the negation of (s_hi - t) + s_lo (IEEE
-// rounding is sign-symmetric), so d^2 is bit-identical to cand_d2().
+// Two candidates per instruction with the sm_100 packed FP32 ops (FADD2, FFMA2, FMUL2):
+// -dx = (t + (-s_hi)) + (-s_lo) is exactly the negation of (s_hi - t) + s_lo (IEEE rounding
+// is sign-symmetric), so d^2 is bit-identical to cand_d2().
 struct NegQuery {
     float2 hx, hy, hz, lx, ly, lz;   // broadcast -s_hi, -s_lo
 };
@@ -151,12 +141,11 @@ __device__ __forceinline__ float2 pair_d2(const NegQuery& q, float2 x, float2 y,
     return __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
 }
 
+// d2[c] for the B candidates of a leaf (padding slots are +inf -> d2 = +inf)
 template <int B>
-__device__ __forceinline__ void eval_leaf(const TargetView& T, const NegQuery& q, int leaf,
-                                          unsigned long long& best, int& bpos) {
-    constexpr int R = B / 4;                                   // float4 per row
+__device__ __forceinline__ void leaf_d2(const TargetView& T, const NegQuery& q, int leaf, float (&d2)[B]) {
+    constexpr int R = B / 4;
     const float4* blk = T.leafsoa + (size_t)leaf * (4 * R);
-    float d2[B];
 #pragma unroll
     for (int c = 0; c < R; ++c) {
         const float4 X = __ldg(blk + c), Y = __ldg(blk + R + c), Z = __ldg(blk + 2 * R + c);
@@ -164,40 +153,75 @@ __device__ __forceinline__ void eval_leaf(const TargetView& T, const NegQuery& q
         const float2 b = pair_d2(q, make_float2(X.z, X.w), make_float2(Y.z, Y.w), make_float2(Z.z, Z.w));
         d2[4 * c + 0] = a.x; d2[4 * c + 1] = a.y; d2[4 * c + 2] = b.x; d2[4 * c + 3] = b.y;
     }
-    float mn = d2[0];
+}
+
+template <int B>
+__device__ __forceinline__ float leaf_min(const float (&d2)[B]) {
+    float m = d2[0];
 #pragma unroll
-    for (int c = 1; c < B; ++c) mn = fminf(mn, d2[c]);
-    if (mn <= key_d2(best)) {                                   // an improvement or a tie is possible
-        // lowest original index among the candidates at the minimum (R1), then one key compare
-        const int* ids = reinterpret_cast<const int*>(blk + 3 * R);
-        uint32_t imin = 0xffffffffu;
-        int cmin = 0;
+    for (int c = 1; c < B; ++c) m = fminf(m, d2[c]);
+    return m;
+}
+
+// lowest original index among the leaf's candidates at d2 == m1 (R1 tie rule)
+template <int B>
+__device__ __forceinline__ uint32_t leaf_argmin(const TargetView& T, int leaf, const float (&d2)[B], float m1) {
+    const int* ids = reinterpret_cast<const int*>(T.leafsoa + (size_t)leaf * B + 3 * (B / 4));
+    uint32_t imin = 0xffffffffu;
 #pragma unroll
-        for (int c = 0; c < B; ++c) {
-            const uint32_t id = (uint32_t)__ldg(ids + c);
-            const bool take = d2[c] == mn && id < imin;
-            imin = take ? id : imin;
-            cmin = take ? c : cmin;
-        }
-        const unsigned long long k = make_key(mn, imin);
-        if (k < best) { best = k; bpos = leaf * B + cmin; }
+    for (int c = 0; c < B; ++c) {
+        const uint32_t id = (uint32_t)__ldg(ids + c);
+        imin = (d2[c] == m1 && id < imin) ? id : imin;
+    }
+    return imin;
+}
+
+// best <- min(best, key of the leaf's nearest candidate); CERT: sec <- the smallest leaf
+// minimum of any OTHER leaf (the value that loses against the running best is pushed:
+// sec <- min(sec, max(best_d2, m1)))
+template <int B, bool CERT>
+__device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuery& q, int leaf,
+                                              unsigned long long& best, float& sec) {
+    float d2[B];
+    leaf_d2<B>(T, q, leaf, d2);
+    const float m1 = leaf_min<B>(d2);
+    if (CERT) sec = fminf(sec, fmaxf(key_d2(best), m1));
+    if (m1 <= key_d2(best)) {
+        const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
+        if (k < best) best = k;
     }
 }
 
-// Morton codes bounding every target that may lie in the ball B(s, sqrt(r2)).
-__device__ __forceinline__ void ball_codes(const float4 Q, const DF3& s, float r2,
-                                           unsigned long long& clo, unsigned long long& chi) {
-    const unsigned qmax = (1u << kMortonBits) - 1u;
-    if (!(r2 < INFINITY)) { clo = 0ull; chi = ~0ull; return; }
-    const float r = sqrtf(r2) * 1.000001f + 1e-30f;
-    unsigned lx = quantize1((s.hx - r) + s.lx, Q.x, Q.w), hx = quantize1((s.hx + r) + s.lx, Q.x, Q.w);
-    unsigned ly = quantize1((s.hy - r) + s.ly, Q.y, Q.w), hy = quantize1((s.hy + r) + s.ly, Q.y, Q.w);
-    unsigned lz = quantize1((s.hz - r) + s.lz, Q.z, Q.w), hz = quantize1((s.hz + r) + s.lz, Q.z, Q.w);
-    // one quantum of margin against rounding in the quantisation of the ball corners
-    lx = lx > 0 ? lx - 1 : 0; ly = ly > 0 ? ly - 1 : 0; lz = lz > 0 ? lz - 1 : 0;
-    hx = hx < qmax ? hx + 1 : qmax; hy = hy < qmax ? hy + 1 : qmax; hz = hz < qmax ? hz + 1 : qmax;
-    clo = morton3(lx, ly, lz);
-    chi = morton3(hx, hy, hz);
+// work-item evaluation (any lane, for a query slot in shared memory): atomicMin on the
+// query's best key; with CERT the key that loses is pushed into the leaf-level 2nd best
+// (linearisable: every leaf minimum that is not the final one is pushed once it loses)
+template <int B, bool CERT>
+__device__ __forceinline__ void eval_leaf_item(const TargetView& T, const NegQuery& q, int leaf,
+                                               unsigned long long* bestS, unsigned* secS) {
+    float d2[B];
+    leaf_d2<B>(T, q, leaf, d2);
+    const float m1 = leaf_min<B>(d2);
+    float push = m1;
+    if (m1 <= key_d2(*(volatile unsigned long long*)bestS)) {
+        const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
+        const unsigned long long old = atomicMin(bestS, k);
+        push = key_d2(old > k ? old : k);
+    }
+    if (CERT && __float_as_uint(push) < *(volatile unsigned*)secS) atomicMin(secS, __float_as_uint(push));
+}
+
+// Lower bound of cand_d2 over the leaf box, bit-identical to box_lb2 (the (lo, hi) pair of
+// an axis goes through one FADD2: x.x = (lo - s_hi) - s_lo, -x.y = (s_hi - hi) + s_lo).
+// lbox[2 leaf] = (lo.x, hi.x, lo.y, hi.y), lbox[2 leaf + 1] = (lo.z, hi.z, 0, 0).
+__device__ __forceinline__ float leaf_lb2(const TargetView& T, const NegQuery& q, int leaf) {
+    const float4 A = __ldg(T.lbox + 2 * (size_t)leaf), Z = __ldg(T.lbox + 2 * (size_t)leaf + 1);
+    const float2 x = __fadd2_rn(__fadd2_rn(make_float2(A.x, A.y), q.hx), q.lx);
+    const float2 y = __fadd2_rn(__fadd2_rn(make_float2(A.z, A.w), q.hy), q.ly);
+    const float2 z = __fadd2_rn(__fadd2_rn(make_float2(Z.x, Z.y), q.hz), q.lz);
+    const float gx = fmaxf(fmaxf(x.x, -x.y), 0.0f);
+    const float gy = fmaxf(fmaxf(y.x, -y.y), 0.0f);
+    const float gz = fmaxf(fmaxf(z.x, -z.y), 0.0f);
+    return fmaf(gx, gx, fmaf(gy, gy, gz * gz));
 }
 
 // Cold-start hint: the leaf holding the target whose Morton key follows the query's own key
@@ -214,144 +238,68 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
     return min(lo, T.n - 1) / T.leaf_size;
 }
 
-// ---------------------------------------------------------------- per-lane search state
-struct NoStats {
-    __device__ __forceinline__ void node() {}
-    __device__ __forceinline__ void leaf() {}
-    __device__ __forceinline__ void level() {}
-};
-struct CountStats {
-    int nodes = 0, leaves = 0, levels = 0;
-    __device__ __forceinline__ void node() { ++nodes; }
-    __device__ __forceinline__ void leaf() { ++leaves; }
-    __device__ __forceinline__ void level() { ++levels; }
-};
-
-constexpr int kMaxDepth = 32;
-
-struct LaneSearch {
-    DF3 s;
-    unsigned long long best;
-    int bpos;
-    int sp;            // DFS stack depth
-    int k;             // ascent level (0 = the hint leaf itself)
-    int u;             // current ancestor node
-    float r2;          // radius^2 the ball codes were computed for
-    unsigned long long clo, chi;
-};
-
-// DFS stack of one lane (local memory, kept apart from the register-resident LaneSearch)
-struct LaneStack {
-    int v[kMaxDepth];
-    float lb[kMaxDepth];
-};
-
-__device__ __forceinline__ void lane_start(LaneSearch& L, const TargetView& T, const DF3& s,
-                                           unsigned long long init, int hint_leaf) {
-    L.s = s;
-    L.best = init;
-    L.bpos = -1;
-    L.sp = 0;
-    L.k = 0;
-    L.u = T.l_pad + hint_leaf;
-    L.r2 = -1.0f;
-}
-
-// Advance this lane's search to the next leaf that must be evaluated; returns the leaf or -1
-// when the search is complete (see the header comment for the ascent / containment rule).
-template <class Stats>
-__device__ __forceinline__ int next_leaf(LaneSearch& L, LaneStack& K, const TargetView& T, Stats* st) {
-    while (true) {
-        if (L.sp > 0) {
-            --L.sp;
-            int v = K.v[L.sp];
-            if (K.lb[L.sp] > key_d2(L.best)) continue;
-            while (v < T.l_pad) {
-                if (st) st->node();
-                const int c = 2 * v;
-                const float4* bx = T.box + 2 * (size_t)c;
-                const float4 lo0 = __ldg(bx + 0), hi0 = __ldg(bx + 1), lo1 = __ldg(bx + 2), hi1 = __ldg(bx + 3);
-                const float lb0 = box_lb2(L.s, lo0, hi0);
-                const float lb1 = box_lb2(L.s, lo1, hi1);
-                const float bd = key_d2(L.best);
-                const bool g0 = lb0 <= bd, g1 = lb1 <= bd;
-                if (g0 && g1) {
-                    const bool right_first = lb1 < lb0;
-                    K.v[L.sp] = right_first ? c : c + 1;
-                    K.lb[L.sp] = right_first ? lb0 : lb1;
-                    ++L.sp;
-                    v = right_first ? c + 1 : c;
-                } else if (g0) {
-                    v = c;
-                } else if (g1) {
-                    v = c + 1;
-                } else {
-                    v = -1;
-                    break;
-                }
-            }
-            if (v >= 0) return v - T.l_pad;
-            continue;
-        }
-        if (L.k >= T.levels) return -1;
-        if (st) st->level();
-        const float bd = key_d2(L.best);
-        if (bd != L.r2) { ball_codes(__ldg(T.quant), L.s, bd, L.clo, L.chi); L.r2 = bd; }
-        const int a = min(((L.u << L.k) - T.l_pad) * T.leaf_size, T.n);
-        const int b = min((((L.u + 1) << L.k) - T.l_pad) * T.leaf_size, T.n);
-        const bool lo_in = a == 0 || __ldg(T.keys + a - 1) < L.clo;
-        const bool hi_in = b >= T.n || L.chi < __ldg(T.keys + b);
-        if (lo_in && hi_in) { L.k = T.levels; return -1; }
-        const int sib = L.u ^ 1;
-        const float lb = node_lb2(T, L.s, sib);
-        ++L.k;
-        L.u >>= 1;
-        if (lb <= bd) {
-            K.v[0] = sib;
-            K.lb[0] = lb;
-            L.sp = 1;
-        }
-    }
-}
-
 // ---------------------------------------------------------------- warp-packet engine
 // A warp takes 32 consecutive queries (one per lane; consecutive = spatially coherent for
 // Morton- or scan-ordered inputs).
-//   A. every lane evaluates its own hint leaf (warm-start match or cold hint): a per-lane
-//      bound r_i = sqrt(best_i).
-//   B. lanes whose r_i is far above the packet mean are "outliers"; the others define the
-//      packet box P = AABB of their balls B(s_i, r_i) (conservatively inflated).
-//   C. breadth-first frontier walk of the BVH: children of the frontier are tested against P,
-//      one box per lane, and compacted with ballots; the last frontier is the list of leaves
-//      whose box meets P -- a superset of the leaves meeting any normal lane's ball.
-//   D. every lane tests every candidate leaf's box against its own ball and appends the
-//      leaves it needs to a private work list (shared memory); the lists are then evaluated in
-//      rounds, each lane gathering its own leaf (packed FP32), so the number of evaluation
-//      rounds is the longest list, not the size of the packet's union.
-//   E. outlier lanes (and whole packets whose frontier overflowed) finish with the exact
-//      ballot DFS: a node is entered iff its lower bound is <= some active lane's best.
+//   A. every lane evaluates its own hint leaf (warm-start match or cold Morton hint): a per-
+//      lane search threshold thr_i = best d2 (with the certificate margin, see CERT below).
+//   B. lanes whose radius is far above the packet mean are "outliers"; the others define the
+//      packet box P = AABB of their balls B(s_i, sqrt(thr_i)) (conservatively inflated).
+//   C. every target inside P has a Morton key in [code(P.lo), code(P.hi)] (the key is
+//      monotone in each quantised coordinate and is computed by the same function), i.e. a
+//      contiguous sorted range [i0, i1) found by two binary searches: the candidate leaves
+//      are the leaves of that range whose box meets P -- tested directly (32 leaves per
+//      step) when the range is short, else by a breadth-first walk (one child box per lane,
+//      ballot compaction) from the lowest common ancestor of the range.
+//   D. every lane tests every candidate leaf against its own ball (lb^2 <= thr); the needed
+//      (leaf, query) pairs are appended, grouped by leaf, to a work list in shared memory.
+//   E. the work list is evaluated 32 items per round (any lane takes any item, so the number
+//      of rounds is sum/32, not the longest per-lane list; lanes of a round mostly share the
+//      leaf and its loads); results merge through shared-memory atomicMin on the u64 keys.
+//   F. outlier lanes (and whole packets whose frontier overflowed) finish with the exact
+//      ballot DFS: a node is entered iff its lower bound is <= some active lane's threshold.
 // Every lane therefore examines every leaf that can hold a target inside its ball: each
 // lane's result is its exact nearest neighbour.
+//
+// CERT (cil_icp_run, SURVEY.md 8(a) a2 certified warm start, leaf form): the threshold is
+// inflated to (sqrt(best) + g)^2 and every lane also keeps sec = the smallest leaf minimum
+// of the evaluated leaves other than the winner's leaf L1.  Every target outside L1 is in an
+// evaluated leaf (d2 >= sec) or in a leaf pruned against the threshold (d2 > thr), so
+// d_out^2 >= min(sec, thr) and the nearest neighbour stays in L1 while the query moves less
+// than (d_out - d1) / 2.
+//
 // Q supplies
 //   __device__ bool load(int i, DF3& s, unsigned long long& init, int& hint_leaf)
-//   __device__ void store(int i, unsigned long long best, int bpos, const DF3& s)
+//   __device__ void store(int i, unsigned long long best, float lb_out2)   (lb_out2 = 0: no certificate)
+//   float gap   (CERT only: the threshold margin g)
 constexpr int kFrontierCap = 256;
-constexpr int kListCap = 8;         // per-lane work-list entries before an evaluation batch
+constexpr int kItemCap = 256;
+constexpr int kDirectLeaves = 256;
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
 template <int B>
 __device__ __forceinline__ void ballot_dfs(const TargetView& T, const DF3& s, const NegQuery& nq, bool on,
-                                           unsigned long long& best, int& bpos) {
+                                           float g, float cap2, unsigned long long& best) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int l_pad = T.l_pad;
-    // lanes that are not searching use a negative radius: no lower bound can pass it
-    const float neg = -1.0f;
+    // lanes that are not searching use a negative threshold: no lower bound can pass it
+    auto thr_of = [&]() {
+        const float d = key_d2(best);
+        if (!on) return -1.0f;
+        if (g == 0.0f) return d;
+        const float r = sqrtf(d) + g;
+        return fmaxf(fminf(r * r, cap2), d);
+    };
     int stk = 0, sp = 0, v = 1;
     while (true) {
-        const float bd = on ? key_d2(best) : neg;
+        const float bd = thr_of();
         if (v >= l_pad) {
-            eval_leaf<B>(T, nq, v - l_pad, best, bpos);
+            // evaluated by the whole (converged) warp; only searching lanes keep the result
+            unsigned long long b2 = best;
+            float s2 = 0.0f;
+            eval_leaf_seq<B, false>(T, nq, v - l_pad, b2, s2);
+            if (on) best = b2;
         } else {
             const int c = 2 * v;
             const float4* bx = T.box + 2 * (size_t)c;
@@ -375,7 +323,7 @@ __device__ __forceinline__ void ballot_dfs(const TargetView& T, const DF3& s, co
             --sp;
             const int cand = __shfl_sync(FULL, stk, sp);
             const float lb = node_lb2(T, s, cand);
-            if (__any_sync(FULL, lb <= (on ? key_d2(best) : neg))) { v = cand; found = true; break; }
+            if (__any_sync(FULL, lb <= thr_of())) { v = cand; found = true; break; }
         }
         if (!found) break;
     }
@@ -385,41 +333,65 @@ __device__ __forceinline__ bool box_meets(float4 lo, float4 hi, float4 plo, floa
     return lo.x <= phi.x && lo.y <= phi.y && lo.z <= phi.z && hi.x >= plo.x && hi.y >= plo.y && hi.z >= plo.z;
 }
 
-template <int B, class Q, class Stats = NoStats>
-__device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int m, unsigned int* counter,
-                                                 Stats* st = nullptr) {
+// first sorted index with key >= code (upper = false) or key > code (upper = true)
+__device__ __forceinline__ int key_bound(const TargetView& T, unsigned long long code, bool upper) {
+    const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
+    int lo = (int)__ldg(T.cell_first + c), hi = (int)__ldg(T.cell_first + c + 1);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const unsigned long long k = __ldg(T.keys + mid);
+        if (upper ? k <= code : k < code) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <int B, bool CERT, class Q>
+__device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int m, unsigned int* counter) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int l_pad = T.l_pad;
-    __shared__ int frontier[kEngineWarps][2][kFrontierCap];
-    __shared__ int worklist[kEngineWarps][1][kListCap * 32];
-    int* F = frontier[threadIdx.x >> 5][0];
-    int* G = frontier[threadIdx.x >> 5][1];
+    __shared__ int sF[kEngineWarps][2][kFrontierCap];
+    __shared__ int sItem[kEngineWarps][kItemCap];
+    __shared__ float sQ[kEngineWarps][6][32];                 // -s_hi, -s_lo per lane
+    __shared__ unsigned long long sBest[kEngineWarps][32];
+    __shared__ unsigned sSec[kEngineWarps][32];
+    int* items = sItem[wid];
+    float g = 0.0f;
+    if constexpr (CERT) g = qs.gap;
     while (true) {
         int base = 0;
         if (lane == 0) base = (int)atomicAdd(counter, 32u);
         base = __shfl_sync(FULL, base, 0);
         if (base >= m) break;
         const int qi = base + lane;
+        const bool tracing = T.trace != nullptr;
+        unsigned ck0 = tracing ? (unsigned)clock() : 0u, ckA = 0, ckB = 0, ckC = 0, ckD = 0;
         DF3 s;
         unsigned long long best = 0ull;
-        int bpos = -1;
         int hint = -1;
         bool active = false;
         if (qi < m) {
             active = qs.load(qi, s, best, hint);
             if (active && hint < 0) hint = coarse_hint_leaf(T, s);
         }
-        if (!active) { s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f; }
+        if (!active) { s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f; best = 0ull; hint = -1; }
         const NegQuery nq = neg_query(s);
+        const float cap2 = key_d2(best);                      // the search bound (rho^2 / max^2 / inf)
+        auto thr_of = [&](unsigned long long b) {
+            const float d = key_d2(b);
+            if (!CERT) return d;
+            const float rr = sqrtf(d) + g;
+            return fmaxf(fminf(rr * rr, cap2), d);
+        };
         // ---- A
-        if (active) {
-            if (st) st->leaf();
-            eval_leaf<B>(T, nq, hint, best, bpos);
-        }
+        float sec = INFINITY;                                 // CERT: leaf-level 2nd best
+        if (active) eval_leaf_seq<B, CERT>(T, nq, hint, best, sec);
+        float thr = active ? thr_of(best) : 0.0f;
+        if (tracing) ckA = (unsigned)clock();
         // ---- B: outliers and the packet box
-        const float r = active ? sqrtf(key_d2(best)) : 0.0f;
+        const float r = active ? sqrtf(thr) : 0.0f;
         float rsum = r;
         int na = active ? 1 : 0;
 #pragma unroll
@@ -428,7 +400,9 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             na += __shfl_xor_sync(FULL, na, o);
         }
         const float rcap = 3.0f * rsum / (float)max(na, 1);
-        const bool normal = active && r <= rcap && r < INFINITY;
+        bool normal = active && r <= rcap && r < INFINITY;
+        if (T.dbg_mode == 1) normal = false;
+        if (T.dbg_mode == 2) normal = active && r < INFINITY;
         const bool outlier = active && !normal;
         // inflate for the double-float offset and for rounding of s_hi -/+ r
         const float rx = r * 1.000001f + fabsf(s.lx) + 1e-6f * fabsf(s.hx) + 1e-30f;
@@ -447,64 +421,138 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             phi.y = fmaxf(phi.y, __shfl_xor_sync(FULL, phi.y, o));
             phi.z = fmaxf(phi.z, __shfl_xor_sync(FULL, phi.z, o));
         }
+        if (tracing) ckB = (unsigned)clock();
         bool overflow = false;
+        int dbg_i0 = -1, dbg_i1 = -1, dbg_nF = -1, dbg_items = 0;
         if (__any_sync(FULL, normal)) {
-            // ---- C: frontier walk from the root against the packet box
-            if (lane == 0) F[0] = 1;
-            __syncwarp();
-            int nF = 1;
-            for (int lev = 0; lev < T.levels && nF > 0; ++lev) {
-                const int nC = 2 * nF;
-                int nN = 0;
-                for (int b0 = 0; b0 < nC; b0 += 32) {
-                    const int j = b0 + lane;
-                    int c = 0;
-                    bool hit = false;
-                    if (j < nC) {
-                        c = 2 * F[j >> 1] + (j & 1);
-                        const float4* bx = T.box + 2 * (size_t)c;
-                        hit = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
-                    }
-                    const unsigned mk = __ballot_sync(FULL, hit);
-                    const int pos = nN + __popc(mk & lt);
-                    if (hit && pos < kFrontierCap) G[pos] = c;
-                    nN += __popc(mk);
-                }
-                __syncwarp();
-                if (st && lane == 0) st->node();
-                if (nN > kFrontierCap) { overflow = true; break; }
-                int* tmp = F; F = G; G = tmp;
-                nF = nN;
+            int* F = sF[wid][0];
+            int* G = sF[wid][1];
+            // ---- C: Morton range of P -> leaf range -> candidate leaves (node ids)
+            int ib = 0;
+            if (lane < 2) {
+                const float4 Qz = __ldg(T.quant);
+                const unsigned long long code = lane == 0 ? morton_of(Qz, plo.x, plo.y, plo.z)
+                                                          : morton_of(Qz, phi.x, phi.y, phi.z);
+                ib = key_bound(T, code, lane == 1);
             }
-            // ---- D: candidate leaves -> per-lane work lists -> gather-evaluation rounds
-            if (!overflow) {
-                int* wl = worklist[threadIdx.x >> 5][0];   // [kListCap][32], lane-major
-                int cnt = 0;
+            const int i0 = __shfl_sync(FULL, ib, 0), i1 = __shfl_sync(FULL, ib, 1);
+            int nF = 0;
+            dbg_i0 = i0; dbg_i1 = i1;
+            if (i1 > i0) {
+                const int la = i0 / B, lb = (i1 - 1) / B;
+                if (lb - la < kDirectLeaves) {
+                    for (int b0 = la; b0 <= lb; b0 += 32) {
+                        const int f = b0 + lane;
+                        bool hit = false;
+                        if (f <= lb) {
+                            const float4* bx = T.box + 2 * (size_t)(l_pad + f);
+                            hit = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
+                        }
+                        const unsigned mk = __ballot_sync(FULL, hit);
+                        if (hit) F[nF + __popc(mk & lt)] = f;
+                        nF += __popc(mk);
+                    }
+                } else {
+                    int a = l_pad + la;
+                    const int k = 32 - __clz(a ^ (l_pad + lb));
+                    a >>= k;
+                    if (lane == 0) F[0] = a;
+                    nF = 1;
+                    __syncwarp();
+                    for (int lev = 0; lev < k && nF > 0; ++lev) {
+                        const int nC = 2 * nF;
+                        int nN = 0;
+                        for (int b0 = 0; b0 < nC; b0 += 32) {
+                            const int j = b0 + lane;
+                            int c = 0;
+                            bool hit = false;
+                            if (j < nC) {
+                                c = 2 * F[j >> 1] + (j & 1);
+                                const float4* bx = T.box + 2 * (size_t)c;
+                                hit = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
+                            }
+                            const unsigned mk = __ballot_sync(FULL, hit);
+                            const int pos = nN + __popc(mk & lt);
+                            if (hit && pos < kFrontierCap) G[pos] = (lev == k - 1) ? c - l_pad : c;
+                            nN += __popc(mk);
+                        }
+                        __syncwarp();
+                        if (nN > kFrontierCap) { overflow = true; break; }
+                        int* tmp = F; F = G; G = tmp;
+                        nF = nN;
+                    }
+                    if (k == 0 && lane == 0) F[0] = a - l_pad;      // the range is one leaf
+                }
+            }
+            __syncwarp();
+            dbg_nF = nF;
+            if (tracing) ckC = (unsigned)clock();
+            // ---- D + E: per-lane need tests -> leaf-grouped work items -> shared rounds
+            if (!overflow && nF > 0) {
+                sQ[wid][0][lane] = -s.hx; sQ[wid][1][lane] = -s.hy; sQ[wid][2][lane] = -s.hz;
+                sQ[wid][3][lane] = -s.lx; sQ[wid][4][lane] = -s.ly; sQ[wid][5][lane] = -s.lz;
+                sBest[wid][lane] = best;
+                if (CERT) sSec[wid][lane] = __float_as_uint(sec);
+                __syncwarp();
+                int nI = 0;
                 for (int k = 0; k < nF; ++k) {
-                    const int v = F[k];
-                    const float lb = node_lb2(T, s, v);
-                    const bool need = normal && lb <= key_d2(best);
-                    if (need) { wl[cnt * 32 + lane] = v - l_pad; ++cnt; }
-                    if (__any_sync(FULL, cnt == kListCap) || k == nF - 1) {
-                        int rounds = cnt;
-#pragma unroll
-                        for (int o = 16; o; o >>= 1) rounds = max(rounds, __shfl_xor_sync(FULL, rounds, o));
-                        for (int q = 0; q < rounds; ++q) {
-                            if (q < cnt) {
-                                if (st) st->leaf();
-                                eval_leaf<B>(T, nq, wl[q * 32 + lane], best, bpos);
+                    const int f = F[k];
+                    const float lb = leaf_lb2(T, nq, f);
+                    const bool need = normal && f != hint && lb <= thr;
+                    const unsigned mk = __ballot_sync(FULL, need);
+                    if (need) items[nI + __popc(mk & lt)] = (f << 5) | lane;
+                    nI += __popc(mk);
+                    if (tracing) dbg_items += need ? 1 : 0;
+                    if (nI > kItemCap - 32 || (k == nF - 1 && nI > 0)) {
+                        __syncwarp();
+                        for (int r0 = 0; r0 < nI; r0 += 32) {
+                            const int j = r0 + lane;
+                            if (j < nI) {
+                                const int it = items[j];
+                                const int q = it & 31;
+                                NegQuery qq;
+                                qq.hx = make_float2(sQ[wid][0][q], sQ[wid][0][q]);
+                                qq.hy = make_float2(sQ[wid][1][q], sQ[wid][1][q]);
+                                qq.hz = make_float2(sQ[wid][2][q], sQ[wid][2][q]);
+                                qq.lx = make_float2(sQ[wid][3][q], sQ[wid][3][q]);
+                                qq.ly = make_float2(sQ[wid][4][q], sQ[wid][4][q]);
+                                qq.lz = make_float2(sQ[wid][5][q], sQ[wid][5][q]);
+                                eval_leaf_item<B, CERT>(T, qq, it >> 5, &sBest[wid][q], &sSec[wid][q]);
                             }
                         }
-                        cnt = 0;
+                        __syncwarp();
+                        nI = 0;
+                        best = sBest[wid][lane];
+                        if (CERT) sec = __uint_as_float(sSec[wid][lane]);
+                        if (active) thr = thr_of(best);
                     }
                 }
             }
-            __syncwarp();
         }
-        // ---- E: exact ballot DFS for outliers (or everyone after an overflow)
+        if (tracing) { ckD = (unsigned)clock(); if (!ckC) ckC = ckD; }
+        int* trace = T.trace;
+        if (trace && qi < m) {
+            int* rec = trace + 16 * (size_t)qi;
+            rec[0] = normal | (outlier << 1) | (overflow << 2);
+            rec[1] = __float_as_int(r);
+            rec[2] = dbg_i0; rec[3] = dbg_i1; rec[4] = dbg_nF;
+            rec[5] = __float_as_int(key_d2(best));
+            rec[6] = dbg_items;
+            rec[8] = (int)(ckA - ck0); rec[9] = (int)(ckB - ckA); rec[10] = (int)(ckC - ckB); rec[11] = (int)(ckD - ckC);
+        }
+        // ---- F: exact ballot DFS for outliers (or everyone after an overflow)
         const bool dfs_on = outlier || (overflow && normal);
-        if (__any_sync(FULL, dfs_on)) ballot_dfs<B>(T, s, nq, dfs_on, best, bpos);
-        if (active) qs.store(qi, best, bpos, s);
+        if (__any_sync(FULL, dfs_on)) ballot_dfs<B>(T, s, nq, dfs_on, g, cap2, best);
+        if (trace && qi < m) {
+            trace[16 * (size_t)qi + 7] = __float_as_int(key_d2(best));
+            trace[16 * (size_t)qi + 12] = (int)((unsigned)clock() - ckD);
+        }
+        if (active) {
+            // targets outside the evaluated leaves are beyond the final threshold
+            const float lb_out2 = (CERT && normal && !overflow) ? fminf(sec, thr) : 0.0f;
+            qs.store(qi, best, lb_out2);
+        }
+        __syncwarp();
     }
 }
 

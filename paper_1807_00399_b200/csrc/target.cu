@@ -7,7 +7,8 @@
 //   K1a bbox partials -> K1b bbox final -> K1c 48-bit Morton key per point
 //   K2  stable LSD radix sort of (key, index) (6 passes x 8 bits: histogram, 3-phase scan,
 //       stable warp-ranked scatter)
-//   K4  gather: sorted float4 (x, y, z, orig index) points and float4 normals
+//   K4  gather: sorted float4 (x, y, z, orig index) points (build temp) and the original-order
+//       float4 points (x, y, z, sorted position) and normals the ICP kernels gather from
 //   K5  leaf AABBs (leaf_size consecutive sorted points) and SoA leaf blocks, then internal
 //       AABBs of an implicit complete binary tree (node v has children 2v, 2v+1), 8 levels per
 //       shared-memory pass; K6 coarse-cell table (first sorted index of every coarse cell).
@@ -167,16 +168,22 @@ __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin,
 }
 
 // ------------------------------------------------------------------ gather + tree
+// sorted points (build temp: x, y, z, orig index) and the ORIGINAL-order copies the ICP
+// kernels gather from: opts[o] = (x, y, z, sorted position), onrm[o] = (nx, ny, nz, 0)
 __global__ void gather_kernel(const float* __restrict__ p, const float* __restrict__ nrm, int n,
-                              const uint32_t* __restrict__ perm, float4* __restrict__ pts, float4* __restrict__ nout) {
+                              const uint32_t* __restrict__ perm, float4* __restrict__ spts,
+                              float4* __restrict__ opts, float4* __restrict__ onrm) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        uint32_t o = perm[i];
-        pts[i] = make_float4(p[3 * (size_t)o], p[3 * (size_t)o + 1], p[3 * (size_t)o + 2], __int_as_float((int)o));
-        if (nout) nout[i] = make_float4(nrm[3 * (size_t)o], nrm[3 * (size_t)o + 1], nrm[3 * (size_t)o + 2], 0.0f);
+        const uint32_t o = perm[i];
+        const float x = p[3 * (size_t)o], y = p[3 * (size_t)o + 1], z = p[3 * (size_t)o + 2];
+        spts[i] = make_float4(x, y, z, __int_as_float((int)o));
+        opts[o] = make_float4(x, y, z, __int_as_float(i));
+        if (onrm) onrm[o] = make_float4(nrm[3 * (size_t)o], nrm[3 * (size_t)o + 1], nrm[3 * (size_t)o + 2], 0.0f);
     }
 }
 
-__global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, int l_pad, float4* __restrict__ box) {
+__global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, int l_pad, float4* __restrict__ box,
+                                int n_leaves, float4* __restrict__ lbox) {
     for (int leaf = blockIdx.x * blockDim.x + threadIdx.x; leaf < l_pad; leaf += gridDim.x * blockDim.x) {
         float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f);
         float4 hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
@@ -189,6 +196,10 @@ __global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, in
         const size_t v = (size_t)l_pad + leaf;
         box[2 * v] = lo;
         box[2 * v + 1] = hi;
+        if (leaf < n_leaves) {
+            lbox[2 * (size_t)leaf] = make_float4(lo.x, hi.x, lo.y, hi.y);
+            lbox[2 * (size_t)leaf + 1] = make_float4(lo.z, hi.z, 0.0f, 0.0f);
+        }
     }
 }
 
@@ -293,7 +304,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     while (coarse_bits < 21 && (1ll << coarse_bits) < n) coarse_bits += 3;
     const int64_t ncell = 1ll << coarse_bits;
 
-    // one allocation: pts (16N), nrm (16N), box (2 * 2*l_pad * 16), keys (8N), cell table, quant
+    // one allocation: opts (16N), onrm (16N), box (2 * 2*l_pad * 16), keys (8N), cell table, quant,
+    // SoA leaves (16N), interleaved leaf boxes (32 per leaf)
     const size_t b_pts = align_up((size_t)N * 16, 256);
     const size_t b_nrm = normals ? align_up((size_t)N * 16, 256) : 0;
     const size_t b_box = align_up((size_t)4 * l_pad * 16, 256);
@@ -301,7 +313,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     const size_t b_cell = align_up((size_t)(ncell + 1) * 4, 256);
     const size_t b_quant = 256;
     const size_t b_soa = align_up((size_t)n_leaves * B * 16, 256);
-    const size_t bytes = b_pts + b_nrm + b_box + b_keys + b_cell + b_quant + b_soa;
+    const size_t b_lbox = align_up((size_t)n_leaves * 32, 256);
+    const size_t bytes = b_pts + b_nrm + b_box + b_keys + b_cell + b_quant + b_soa + b_lbox;
     int dev = 0;
     CIL_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
     void* mem = nullptr;
@@ -314,6 +327,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     uint32_t* d_cell = (uint32_t*)(base + b_pts + b_nrm + b_box + b_keys);
     float4* d_quant = (float4*)(base + b_pts + b_nrm + b_box + b_keys + b_cell);
     float* d_soa = (float*)(base + b_pts + b_nrm + b_box + b_keys + b_cell + b_quant);
+    float4* d_lbox = (float4*)(base + b_pts + b_nrm + b_box + b_keys + b_cell + b_quant + b_soa);
 
     // scratch: keys x2 (8N), vals x2 (4N), hist (256 * nblk), bbox partials
     const int nblk_sort = (N + kTile - 1) / kTile;
@@ -322,7 +336,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
     const size_t s_bb = align_up((size_t)(6 * nblk_bbox) * 4, 256);
     const size_t s_scan = scan_temp_bytes((int64_t)kRadix * nblk_sort);
-    const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb + s_scan;
+    const size_t s_spts = align_up((size_t)N * 16, 256);
+    const size_t scratch = 2 * s_keys + 2 * s_vals + s_hist + s_bb + s_scan + s_spts;
     void* tmp = nullptr;
     cudaError_t e = pool_alloc(&tmp, scratch, s);
     if (e != cudaSuccess) { pool_free(mem, s); return cuda_fail(e, "pool_alloc(scratch)"); }
@@ -334,6 +349,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     uint32_t* hist = (uint32_t*)(tb + 2 * s_keys + 2 * s_vals);
     float* bbp = (float*)(tb + 2 * s_keys + 2 * s_vals + s_hist);
     void* scan_tmp = (void*)(tb + 2 * s_keys + 2 * s_vals + s_hist + s_bb);
+    float4* spts = (float4*)(tb + 2 * s_keys + 2 * s_vals + s_hist + s_bb + s_scan);
     int nlaunch = 0;
 
     prof_begin(kProfBuild, s);
@@ -347,11 +363,11 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
         std::swap(k0, k1);
         std::swap(v0, v1);
     }
-    gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, d_pts, d_nrm);
+    gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, spts, d_pts, d_nrm);
     cudaMemcpyAsync(d_keys, k0, (size_t)N * 8, cudaMemcpyDeviceToDevice, s);
     cell_first_kernel<<<grid_for(ncell + 1), kThreads, 0, s>>>(k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
-    leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(d_pts, N, B, (int)l_pad, d_box);
-    leaf_soa_kernel<<<grid_for(n_leaves * B), kThreads, 0, s>>>(d_pts, N, B, n_leaves, d_soa);
+    leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(spts, N, B, (int)l_pad, d_box, (int)n_leaves, d_lbox);
+    leaf_soa_kernel<<<grid_for(n_leaves * B), kThreads, 0, s>>>(spts, N, B, n_leaves, d_soa);
     int tree_passes = 0;
     for (int first = (int)l_pad, rem = levels; rem > 0; ++tree_passes) {
         const int lv = std::min(rem, 8);
@@ -367,18 +383,21 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     if (e != cudaSuccess) { pool_free(mem, s); return cuda_fail(e, "cil_target_build launch"); }
 
     cil_target* t = new cil_target;
-    t->v.pts = d_pts;
-    t->v.nrm = d_nrm;
+    t->v.opts = d_pts;
+    t->v.onrm = d_nrm;
     t->v.box = d_box;
     t->v.n = N;
     t->v.l_pad = (int)l_pad;
     t->v.leaf_size = B;
     t->v.keys = d_keys;
     t->v.leafsoa = (const float4*)d_soa;
+    t->v.lbox = d_lbox;
     t->v.cell_first = d_cell;
     t->v.quant = d_quant;
     t->v.levels = levels;
     t->v.coarse_bits = coarse_bits;
+    t->v.trace = nullptr;
+    t->v.dbg_mode = 0;
     t->n_leaves = n_leaves;
     t->has_normals = normals ? 1 : 0;
     t->device = dev;

@@ -46,6 +46,7 @@ struct IterArgs {
     float search2;           // search bound: bound2, or fl32(rho^2) with certificates
     float gap_none;          // certificate of "no target within rho": rho - max_corr_dist (rounded down)
     float cert_gap;          // search-threshold margin g of the leaf certificate
+    float stale2;            // (max_corr_dist / 10)^2: a warm hint beyond it is stale
     const double* pose_in;
     double* pose_out;
     double* partials;        // [kMaxCtas * kSlots]
@@ -54,9 +55,11 @@ struct IterArgs {
     int32_t* corr_idx;       // iterate only, nullable
     float* corr_d2;          // iterate only, nullable
     int* nn;                 // [m] match per query (original target index or -1)
-    uint32_t* gw;            // [m] gap word (run): bits(gap) & ~255 | anchor slot
-    int* list;               // [m] uncertified queries of this iteration (run with certificates)
-    unsigned long long* sel_status;   // [tiles] chained-scan status of K_sel (run)
+    uint32_t* gw;            // [m] leaf-certificate word (run): bits(G1) & ~255 | anchor slot
+    float* gs;               // [m] list-certificate margin G_S (run)
+    int* vlist;              // [m][kListLeaves] candidate leaves of the last search (run), -1 padded
+    uint32_t* pmask;         // [ceil(m/32)] per 32-query packet: lanes that need a full search (run)
+    int* plist;              // [ceil(m/32)] packets with a non-empty mask (any order; count st->plist_n)
     double* apose;           // [kAnchorSlots][12] pose of each anchor slot (run)
     float* adelta;           // [kAnchorSlots][16] (R - R_a | t - t_a | max|dR| | max|dt|) for the current pose
     double* iter_log;        // run only, nullable
@@ -235,76 +238,157 @@ __device__ __forceinline__ float displacement_bound(const float* __restrict__ D,
     return fmaf(nv, 1.0f + 0x1p-20f, fmaf(0x1p-19f, fmaf(d3.x, p1, d3.y), 0x1p-30f * (p1 + 1.0f)));
 }
 
-// Order-preserving compaction (the list keeps source order, so a 32-query packet of the
-// search stays spatially coherent): one tile of kSelTile consecutive queries per CTA, tile
-// ids from a ticket (so every lower tile is already running), single-pass chained scan
-// with decoupled look-back over per-tile status words (epoch | flag | count) in one u64.
+// K_sel writes, per packet of 32 consecutive source points, the mask of the points that need
+// a full search; K_nn then runs its packets in source order with only those lanes active, so
+// an uncertified remainder stays spatially coherent (a compacted list would scatter it).
 constexpr int kSelThreads = 256;
-constexpr int kSelRounds = 8;
-constexpr int kSelTile = kSelThreads * kSelRounds;     // 2048 queries per tile
+constexpr int kSelRounds = 2;
+constexpr int kSelTile = kSelThreads * kSelRounds;     // 512 queries per CTA
 
-__device__ __forceinline__ bool needs_search(const IterArgs& a, int i, uint32_t kslot) {
-    const uint32_t w = a.gw[i];
-    const float G = __uint_as_float(w & ~255u);
-    const uint32_t slot = w & 255u;
-    // slot == kslot only after 256 iterations: that anchor pose is being recycled
-    if (!(G > 0.0f) || slot == kslot) return true;
-    const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
-    const float D = displacement_bound(a.adelta + 16 * slot, px, py, pz);
-    return a.nn[i] >= 0 ? !(G > 2.0f * D) : !(G > D);
+// Certificates of query i at the current pose, one query per lane, the
+// whole warp together: returns true if the lane's query needs a full search; otherwise its
+// exact nearest neighbour is found here and written to nn[i]:
+//   leaf certificate  G1 > 2 D : the NN is in the previous match's leaf L1;
+//   list certificate  G_S > 2 D: the NN is in the stored candidate-leaf list (a Verlet list
+//                                with skin g: every other target was beyond r_S = d1 + G_S);
+//   nothing within rho, G1 = rho - max_corr_dist > D: still nothing within max_corr_dist.
+// The (query, leaf) evaluations of the warp are flattened into rounds of 32 independent
+// items (shared-memory atomicMin on the queries' u64 keys), so a warp keeps 32 leaf loads
+// in flight instead of walking each lane's list in sequence.
+struct SelWarp {
+    float q[6][32];                          // -s_hi, -s_lo per lane
+    unsigned long long best[32];
+    int items[32 * kListLeaves];
+};
+
+template <int B>
+__device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P, int i, uint32_t kslot, SelWarp& S) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    bool need = false;
+    int nit = 0, j = -1;
+    int4 l0 = make_int4(-1, -1, -1, -1), l1 = make_int4(-1, -1, -1, -1);
+    if (i < a.m) {
+        const uint32_t w = a.gw[i];
+        // slot == kslot: never anchored (iteration 0) or an anchor pose being recycled (k >= 256)
+        if ((w & 255u) == kslot) {
+            need = true;
+        } else {
+            const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
+            const float D = displacement_bound(a.adelta + 16 * (w & 255u), px, py, pz);
+            const float G1 = __uint_as_float(w & ~255u);
+            j = a.nn[i];
+            if (j < 0) {
+                need = !(G1 > D);
+            } else {
+                const bool leaf_ok = G1 > 2.0f * D;
+                if (leaf_ok || a.gs[i] > 2.0f * D) {
+                    const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
+                    l0 = vl[0];
+                    if (!leaf_ok) l1 = vl[1];
+                    nit = leaf_ok ? 1
+                                  : (l0.x >= 0) + (l0.y >= 0) + (l0.z >= 0) + (l0.w >= 0) + (l1.x >= 0) +
+                                        (l1.y >= 0) + (l1.z >= 0) + (l1.w >= 0);
+                    const DF3 s = transform_df(P, px, py, pz);
+                    S.q[0][lane] = -s.hx; S.q[1][lane] = -s.hy; S.q[2][lane] = -s.hz;
+                    S.q[3][lane] = -s.lx; S.q[4][lane] = -s.ly; S.q[5][lane] = -s.lz;
+                    S.best[lane] = bound_key(INFINITY);
+                } else {
+                    need = true;
+                }
+            }
+        }
+    }
+    // phase 1: L1 (the anchor match's leaf, entry 0) of every certified lane -- usually the
+    // winner; phase 2: the rest of the lists, flattened into rounds of 32 (query, leaf) items,
+    // each evaluated only if the leaf box can still beat the query's current best
+    const CertSlots none{};
+    NegQuery nq0;
+    if (nit > 0) {
+        nq0.hx = make_float2(S.q[0][lane], S.q[0][lane]); nq0.hy = make_float2(S.q[1][lane], S.q[1][lane]);
+        nq0.hz = make_float2(S.q[2][lane], S.q[2][lane]); nq0.lx = make_float2(S.q[3][lane], S.q[3][lane]);
+        nq0.ly = make_float2(S.q[4][lane], S.q[4][lane]); nq0.lz = make_float2(S.q[5][lane], S.q[5][lane]);
+        eval_leaf_item<B, false>(a.T, nq0, l0.x, &S.best[lane], none);
+    }
+    const int rest = nit > 1 ? nit - 1 : 0;
+    int incl = rest;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    const int excl = incl - rest;
+    const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+    for (int c = 1; c < kListLeaves; ++c)
+        if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
+    __syncwarp();
+    for (int r0 = 0; r0 < total; r0 += 32) {
+        const int k = r0 + lane;
+        if (k < total) {
+            const int it = S.items[k];
+            const int q = it & 31;
+            NegQuery qq;
+            qq.hx = make_float2(S.q[0][q], S.q[0][q]);
+            qq.hy = make_float2(S.q[1][q], S.q[1][q]);
+            qq.hz = make_float2(S.q[2][q], S.q[2][q]);
+            qq.lx = make_float2(S.q[3][q], S.q[3][q]);
+            qq.ly = make_float2(S.q[4][q], S.q[4][q]);
+            qq.lz = make_float2(S.q[5][q], S.q[5][q]);
+            if (leaf_lb2(a.T, qq, it >> 5) <= key_d2(*(volatile unsigned long long*)&S.best[q]))
+                eval_leaf_item<B, false>(a.T, qq, it >> 5, &S.best[q], none);
+        }
+    }
+    __syncwarp();
+    if (nit > 0) {
+        const int jn = (int)key_idx(S.best[lane]);
+        if (jn != j) a.nn[i] = jn;
+    }
+    __syncwarp();
+    return need;
 }
 
+template <int B>
 __global__ void __launch_bounds__(kSelThreads)
 icp_select_kernel(const IterArgs a) {
-    __shared__ int s_tile, s_base;
-    __shared__ int s_wsum[kSelThreads / 32];
+    __shared__ SelWarp s_w[kSelThreads / 32];
+    __shared__ double s_pose[12];
+    __shared__ int s_cnt, s_np, s_base;
+    __shared__ int s_pk[kSelTile / 32];
     if (*(volatile int*)&a.st->done) return;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    const int k = *(volatile int*)&a.st->iters;
-    const uint32_t kslot = (uint32_t)k & (kAnchorSlots - 1);
-    const unsigned long long epoch = (unsigned long long)((k + 1) & 0xffff);
-    if (threadIdx.x == 0) s_tile = atomicAdd(&a.st->sel_ticket, 1);
+    const uint32_t kslot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
+    if (threadIdx.x < 12) s_pose[threadIdx.x] = a.st->pose[threadIdx.x];
+    if (threadIdx.x == 0) { s_cnt = 0; s_np = 0; }
     __syncthreads();
-    const int tile = s_tile;
-    const int wbase = tile * kSelTile + warp * (32 * kSelRounds);
-    unsigned masks[kSelRounds];
+    Pose34 P;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) P.r[e] = s_pose[e];
+    const int wbase = blockIdx.x * kSelTile + warp * (32 * kSelRounds);
     int cnt = 0;
 #pragma unroll
     for (int r = 0; r < kSelRounds; ++r) {
-        const int i = wbase + 32 * r + lane;
-        masks[r] = __ballot_sync(FULL, i < a.m && needs_search(a, i, kslot));
-        cnt += __popc(masks[r]);
-    }
-    if (lane == 0) s_wsum[warp] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int tot = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) { const int c = s_wsum[w]; s_wsum[w] = tot; tot += c; }
-        unsigned long long* stat = a.sel_status;
-        int excl = 0;
-        if (tile > 0) {
-            atomicExch(stat + tile, (epoch << 48) | (1ull << 32) | (unsigned)tot);
-            for (int p = tile - 1; p >= 0;) {
-                const unsigned long long v = *(volatile unsigned long long*)(stat + p);
-                if ((v >> 48) != epoch) continue;                       // predecessor not published yet
-                excl += (int)(v & 0xffffffffull);
-                if (((v >> 32) & 3ull) == 2ull) break;                  // inclusive prefix: done
-                --p;
-            }
+        const int i0 = wbase + 32 * r;
+        if (i0 >= a.m) break;
+        const unsigned mk = __ballot_sync(FULL, certify_warp<B>(a, P, i0 + lane, kslot, s_w[warp]));
+        if (lane == 0) {
+            a.pmask[i0 >> 5] = mk;
+            if (mk) s_pk[atomicAdd(&s_np, 1)] = i0 >> 5;
         }
-        atomicExch(stat + tile, (epoch << 48) | (2ull << 32) | (unsigned)(excl + tot));
-        if (tile == (int)gridDim.x - 1) a.st->list_n = excl + tot;
-        s_base = excl;
+        cnt += __popc(mk);
+    }
+    if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    // packets that need a search go to the list (one global atomic per CTA; any order: a
+    // packet is a self-contained, spatially coherent unit)
+    if (threadIdx.x == 0) {
+        s_base = s_np ? atomicAdd(&a.st->plist_n, s_np) : 0;
+        if (s_cnt) atomicAdd(&a.st->list_n, s_cnt);                    // diagnostics: searched points
     }
     __syncthreads();
-    int pos = s_base + s_wsum[warp];
-#pragma unroll
-    for (int r = 0; r < kSelRounds; ++r) {
-        if ((masks[r] >> lane) & 1u) a.list[pos + __popc(masks[r] & lt)] = wbase + 32 * r + lane;
-        pos += __popc(masks[r]);
-    }
+    if (threadIdx.x < s_np) a.plist[s_base + threadIdx.x] = s_pk[threadIdx.x];
 }
 
 // ---------------------------------------------------------------- K_nn
@@ -318,40 +402,75 @@ struct IcpQueries {
     float search2;
     float gap_none;
     float gap;               // CERT: search-threshold margin g (leaf form)
+    float stale2;            // a warm hint farther than this (d^2) is complemented by the cold hint
     int* nn;
     uint32_t* gw;
-    const int* list;
+    float* gs;
+    int* vlist;
+    const uint32_t* pmask;
+    const int* plist;        // CERT: packets with a non-empty mask, count at *plist_n
+    const int* plist_n;
     int warm;
     uint32_t slot;
     int32_t* corr_idx;
     float* corr_d2;
-    __device__ __forceinline__ bool load(int k, DF3& s, unsigned long long& init, int& hint) const {
-        const int i = list ? list[k] : k;
+    __device__ __forceinline__ int packets(int m) const { return plist ? *(volatile const int*)plist_n : (m + 31) / 32; }
+    __device__ __forceinline__ int packet_base(int c) const { return 32 * (plist ? plist[c] : c); }
+    __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
+        if (pmask && !((pmask[i >> 5] >> (i & 31)) & 1u)) return false;    // certified in K_sel
         s = transform_df(P, src[3 * (size_t)i], src[3 * (size_t)i + 1], src[3 * (size_t)i + 2]);
         init = bound_key(search2);
         const int j = warm ? nn[i] : -1;
         hint = j >= 0 ? __float_as_int(__ldg(&opts[j].w)) / B : -1;
         return true;
     }
-    __device__ __forceinline__ void store(int k, unsigned long long best, float lb_out2) const {
-        const int i = list ? list[k] : k;
+    __device__ __forceinline__ void store(int i, unsigned long long best, float) const {
         const bool found = best != bound_key(search2);
         nn[i] = found ? (int)key_idx(best) : -1;
-        if (CERT) {
-            // leaf certificate G = d_out - d1: every target outside the winner's leaf is at
-            // fp32 distance >= sqrt(lb_out2); 4e-6 relative slack covers the fp32 d^2 error,
-            // rounded toward zero by clearing the low 8 bits (they hold the anchor slot)
-            float G = gap_none;
-            if (found) G = fmaxf(sqrtf(lb_out2) * (1.0f - 4e-6f) - sqrtf(key_d2(best)) * (1.0f + 4e-6f), 0.0f);
-            gw[i] = (__float_as_uint(G) & ~255u) | slot;
-        }
         if (corr_idx) corr_idx[i] = found ? (int32_t)key_idx(best) : -1;
         if (corr_d2) corr_d2[i] = found ? key_d2(best) : INFINITY;
+    }
+    // CERT: the certificates of the new anchor (this iteration's pose).  G1 = d_out - d1 (leaf
+    // form), G_S = r_S - d1 (candidate-leaf list); 4e-6 relative slack covers the fp32 d^2
+    // error; G1 is rounded toward zero by clearing the low 8 bits (they hold the anchor slot).
+    __device__ __forceinline__ void store(int i, unsigned long long best, float lb_out2, const int* lst, int cnt,
+                                          float rS2) const {
+        const bool found = best != bound_key(search2);
+        nn[i] = found ? (int)key_idx(best) : -1;
+        float G1 = gap_none, GS = 0.0f;
+        if (found) {
+            const float d1 = sqrtf(key_d2(best)) * (1.0f + 4e-6f);
+            G1 = fmaxf(sqrtf(lb_out2) * (1.0f - 4e-6f) - d1, 0.0f);
+            GS = cnt > 0 ? fmaxf(sqrtf(rS2) * (1.0f - 4e-6f) - d1, 0.0f) : 0.0f;
+        }
+        gw[i] = (__float_as_uint(G1) & ~255u) | slot;
+        gs[i] = GS;
+        // entry 0 = L1, the anchor match's leaf (the leaf certificate refers to it even after a
+        // list-certified iteration moved the match to another leaf), then the rest of the list
+        const int L1 = found ? __float_as_int(__ldg(&opts[key_idx(best)].w)) / B : -1;
+        int e[kListLeaves];
+        e[0] = L1;
+        int n = 1;
+        bool has_L1 = false;
+#pragma unroll
+        for (int c = 0; c < kListLeaves; ++c) {
+            const int v = c < cnt ? lst[c] : -1;
+            has_L1 |= v == L1;
+            if (v >= 0 && v != L1 && n < kListLeaves) e[n++] = v;
+        }
+#pragma unroll
+        for (int c = 1; c < kListLeaves; ++c) if (c >= n) e[c] = -1;
+        // no list, or L1 missing from a full list (an entry would be lost): no list certificate
+        if (cnt == 0 || (!has_L1 && cnt == kListLeaves)) GS = 0.0f;
+        const int4 l0 = make_int4(e[0], e[1], e[2], e[3]), l1 = make_int4(e[4], e[5], e[6], e[7]);
+        int4* dst = reinterpret_cast<int4*>(vlist + (size_t)kListLeaves * i);
+        dst[0] = l0;
+        dst[1] = l1;
     }
 };
 
 template <int B, bool CERT>
-__global__ void __launch_bounds__(kNNThreads)
+__global__ void __launch_bounds__(kNNThreads, 4)
 icp_nn_kernel(const IterArgs a) {
     if (a.run && *(volatile int*)&a.st->done) return;
     IcpQueries<B, CERT> qs;
@@ -362,20 +481,24 @@ icp_nn_kernel(const IterArgs a) {
     qs.search2 = a.search2;
     qs.gap_none = a.gap_none;
     qs.gap = a.cert_gap;
+    qs.stale2 = a.stale2;
     qs.nn = a.nn;
     qs.gw = a.gw;
-    qs.list = a.cert ? a.list : nullptr;
+    qs.gs = a.gs;
+    qs.vlist = a.vlist;
+    qs.pmask = a.cert ? a.pmask : nullptr;
+    qs.plist = a.cert ? a.plist : nullptr;
+    qs.plist_n = &a.st->plist_n;
     qs.warm = a.run;
     qs.slot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     qs.corr_idx = a.corr_idx;
     qs.corr_d2 = a.corr_d2;
-    const int m = a.cert ? *(volatile int*)&a.st->list_n : a.m;
-    nn_packet_engine<B, CERT>(a.T, qs, m, &a.st->work);
+    nn_packet_engine<B, CERT>(a.T, qs, a.m, &a.st->work);
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
-template <int METRIC, int B>
-__global__ void __launch_bounds__(kIcpThreads)
+template <int METRIC>
+__global__ void __launch_bounds__(kIcpThreads, 3)
 icp_acc_kernel(const IterArgs a) {
     __shared__ double wsum[kIcpWarps][kSlots];
     __shared__ double Ssum[kSlots];
@@ -394,30 +517,15 @@ icp_acc_kernel(const IterArgs a) {
     for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
 
     const TargetView& T = a.T;
-    const int stride = gridDim.x * blockDim.x;
-    const uint32_t kslot = a.cert ? ((uint32_t)a.st->iters & (kAnchorSlots - 1)) : 0u;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += stride) {
-        int j = a.nn[i];
-        if (j < 0) continue;                                            // a3: nothing within the bound
-        const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1],
-                                   a.src[3 * (size_t)i + 2]);            // a1
-        float4 t = __ldg(T.opts + j);
-        if (a.cert && (a.gw[i] & 255u) != kslot) {
-            // certified (K_sel): the exact nearest neighbour lies in the previous match's leaf
-            const int leaf = __float_as_int(t.w) / B;
-            const NegQuery nq = neg_query(s);
-            float d2[B];
-            leaf_d2<B>(T, nq, leaf, d2);
-            const float m1 = leaf_min<B>(d2);
-            const int jn = (int)leaf_argmin<B>(T, leaf, d2, m1);
-            if (jn != j) { a.nn[i] = jn; j = jn; t = __ldg(T.opts + j); }
-        }
+    // a1 + a3 + a4 + a5 for the pair (p, t_j): transform, inclusive rejection (R2), residual,
+    // Jacobian, fp32 per-thread sums
+    auto pair = [&](float px, float py, float pz, float4 t, float4 n) {
+        const DF3 s = transform_df(P, px, py, pz);
         const float dx = dfdiff(s.hx, s.lx, t.x);
         const float dy = dfdiff(s.hy, s.ly, t.y);
         const float dz = dfdiff(s.hz, s.lz, t.z);
-        if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= a.bound2)) continue;   // a3 (inclusive, R2)
-        if (METRIC == CIL_POINT_TO_PLANE) {                             // a4 + a5
-            const float4 n = __ldg(T.onrm + j);
+        if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= a.bound2)) return;
+        if (METRIC == CIL_POINT_TO_PLANE) {
             const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
             const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
                                 fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
@@ -442,6 +550,29 @@ icp_acc_kernel(const IterArgs a) {
             acc[15] += fmaf(sx, dy, -sy * dx);
             acc[16] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, acc[16])));
         }
+    };
+    // two queries per trip with every load issued before the arithmetic (the gathers depend on
+    // nn[]; two independent chains in flight per thread); summation order = grid-stride order
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += 2 * stride) {
+        const int i1 = i + stride;
+        const int j0 = a.nn[i];
+        const int j1 = i1 < a.m ? a.nn[i1] : -1;
+        const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        float4 t0 = z4, t1 = z4, n0 = z4, n1 = z4;
+        float p0x = 0.0f, p0y = 0.0f, p0z = 0.0f, p1x = 0.0f, p1y = 0.0f, p1z = 0.0f;
+        if (j0 >= 0) {
+            t0 = __ldg(T.opts + j0);
+            if (METRIC == CIL_POINT_TO_PLANE) n0 = __ldg(T.onrm + j0);
+            p0x = a.src[3 * (size_t)i]; p0y = a.src[3 * (size_t)i + 1]; p0z = a.src[3 * (size_t)i + 2];
+        }
+        if (j1 >= 0) {
+            t1 = __ldg(T.opts + j1);
+            if (METRIC == CIL_POINT_TO_PLANE) n1 = __ldg(T.onrm + j1);
+            p1x = a.src[3 * (size_t)i1]; p1y = a.src[3 * (size_t)i1 + 1]; p1z = a.src[3 * (size_t)i1 + 2];
+        }
+        if (j0 >= 0) pair(p0x, p0y, p0z, t0, n0);                       // a3: j < 0 = nothing within the bound
+        if (j1 >= 0) pair(p1x, p1y, p1z, t1, n1);
     }
 
     // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
@@ -485,7 +616,7 @@ icp_acc_kernel(const IterArgs a) {
         a.st->work = 0;      // K_nn's counter, for the next iteration
         a.st->searched += a.run ? a.st->list_n : 0;
         a.st->list_n = 0;
-        a.st->sel_ticket = 0;
+        a.st->plist_n = 0;
     }
     __syncthreads();
     // anchor table for the next iteration's K_sel: delta of every live slot to the new pose
@@ -517,14 +648,13 @@ icp_acc_kernel(const IterArgs a) {
 
 // ---------------------------------------------------------------- run bookkeeping kernels
 __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, uint32_t* gw, int m,
-                                unsigned long long* sel_status, double* iter_log, int log_len) {
+                                double* iter_log, int log_len) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0) {
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
-        st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->sel_ticket = 0;
+        st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
     }
-    for (int i = tid; i < (m + kSelTile - 1) / kSelTile; i += gridDim.x * blockDim.x) sel_status[i] = 0ull;
     for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; }
     if (iter_log)
         for (int i = tid; i < log_len; i += gridDim.x * blockDim.x) iter_log[i] = 0.0;
@@ -579,24 +709,14 @@ cudaError_t launch_nn_t(const IterArgs& a, cudaStream_t s) {
     }
 }
 
-template <int METRIC, int B>
-cudaError_t launch_acc_mb(const IterArgs& a, cudaStream_t s) {
-    static const int occ = occupancy_of(icp_acc_kernel<METRIC, B>, kIcpThreads);
-    const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
-    prof_begin(kProfAcc, s);
-    icp_acc_kernel<METRIC, B><<<g, kIcpThreads, 0, s>>>(a);
-    prof_end(s);
-    return cudaGetLastError();
-}
-
 template <int METRIC>
 cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
-    switch (a.T.leaf_size) {
-        case 4: return launch_acc_mb<METRIC, 4>(a, s);
-        case 8: return launch_acc_mb<METRIC, 8>(a, s);
-        case 16: return launch_acc_mb<METRIC, 16>(a, s);
-        default: return launch_acc_mb<METRIC, 32>(a, s);
-    }
+    static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads);
+    const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
+    prof_begin(kProfAcc, s);
+    icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
+    prof_end(s);
+    return cudaGetLastError();
 }
 
 // one ICP iteration = [K_sel] + K_nn + K_acc
@@ -605,7 +725,12 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
     if (a.cert) {
         const int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
         prof_begin(kProfSel, s);
-        icp_select_kernel<<<g, kSelThreads, 0, s>>>(a);
+        switch (a.T.leaf_size) {
+            case 4: icp_select_kernel<4><<<g, kSelThreads, 0, s>>>(a); break;
+            case 8: icp_select_kernel<8><<<g, kSelThreads, 0, s>>>(a); break;
+            case 16: icp_select_kernel<16><<<g, kSelThreads, 0, s>>>(a); break;
+            default: icp_select_kernel<32><<<g, kSelThreads, 0, s>>>(a); break;
+        }
         prof_end(s);
         ++n;
     }
@@ -617,7 +742,7 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
 }
 
 struct WsLayout {
-    size_t state, partials, apose, adelta, nn, gw, list, sel, total;
+    size_t state, partials, apose, adelta, nn, gw, pmask, plist, gs, vlist, total;
 };
 
 WsLayout ws_layout(int64_t m) {
@@ -629,9 +754,11 @@ WsLayout ws_layout(int64_t m) {
     L.adelta = L.apose + align_up((size_t)kAnchorSlots * 12 * sizeof(double), 256);
     L.nn = L.adelta + align_up((size_t)kAnchorSlots * 16 * sizeof(float), 256);
     L.gw = L.nn + align_up(mm * sizeof(int), 256);
-    L.list = L.gw + align_up(mm * sizeof(uint32_t), 256);
-    L.sel = L.list + align_up(mm * sizeof(int), 256);
-    L.total = L.sel + align_up((mm + kSelTile - 1) / kSelTile * sizeof(unsigned long long), 256);
+    L.pmask = L.gw + align_up(mm * sizeof(uint32_t), 256);
+    L.plist = L.pmask + align_up((mm + 31) / 32 * sizeof(uint32_t), 256);
+    L.gs = L.plist + align_up((mm + 31) / 32 * sizeof(int), 256);
+    L.vlist = L.gs + align_up(mm * sizeof(float), 256);
+    L.total = L.vlist + align_up(mm * kListLeaves * sizeof(int), 256);
     return L;
 }
 
@@ -644,8 +771,10 @@ void bind_ws(IterArgs& a, void* ws, int64_t m) {
     a.adelta = (float*)(w + L.adelta);
     a.nn = (int*)(w + L.nn);
     a.gw = (uint32_t*)(w + L.gw);
-    a.list = (int*)(w + L.list);
-    a.sel_status = (unsigned long long*)(w + L.sel);
+    a.pmask = (uint32_t*)(w + L.pmask);
+    a.plist = (int*)(w + L.plist);
+    a.gs = (float*)(w + L.gs);
+    a.vlist = (int*)(w + L.vlist);
 }
 
 cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
@@ -741,6 +870,7 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     }
     // leaf-certificate margin g: the search threshold of K_nn is (sqrt(best) + g)^2
     a.cert_gap = (float)(cert_gap_frac() * (std::isinf(params->max_corr_dist) ? 0.0 : params->max_corr_dist));
+    a.stale2 = std::isinf(params->max_corr_dist) ? INFINITY : (float)(0.01 * params->max_corr_dist * params->max_corr_dist);
     a.pose_in = a.st->pose;
     a.pose_out = a.st->pose;
     a.iter_log = iter_log;
@@ -749,7 +879,7 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.trans_tol = params->trans_tol;
     cudaStream_t s = (cudaStream_t)stream;
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
-    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, (int)m, a.sel_status, iter_log,
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, (int)m, iter_log,
                                                 2 * params->max_iters);
     count_launches(1);
     cudaError_t e = cudaGetLastError();

@@ -58,8 +58,8 @@ struct alignas(256) IcpState {
     int done;             // 156
     unsigned int ticket;  // 160: last-CTA ticket of the accumulation kernel
     unsigned int work;    // 164: dynamic work counter of the search kernel
-    int list_n;           // 168: uncertified queries of the running iteration (search list size)
-    int sel_ticket;       // 172: tile ticket of the selection kernel
+    int list_n;           // 168: uncertified queries of the running iteration (diagnostics)
+    int plist_n;          // 172: packets in the search list of the running iteration
     long long searched;   // 176: sum over executed iterations of list_n (diagnostics)
 };
 

@@ -18,8 +18,11 @@ struct NNQueries {
     const float* q;
     const uint32_t* perm;
     float bound2;
+    float stale2;            // unused (no warm hints)
     int32_t* idx;
     float* sqd;
+    __device__ __forceinline__ int packets(int m) const { return (m + 31) / 32; }
+    __device__ __forceinline__ int packet_base(int c) const { return 32 * c; }
     __device__ __forceinline__ bool load(int k, DF3& s, unsigned long long& init, int& hint) const {
         const size_t i = perm[k];
         s.hx = q[3 * i]; s.hy = q[3 * i + 1]; s.hz = q[3 * i + 2];
@@ -55,7 +58,7 @@ __global__ void qcell_scatter_kernel(const uint32_t* __restrict__ qcell, int m, 
 }
 
 template <int B>
-__global__ void __launch_bounds__(kNNThreads)
+__global__ void __launch_bounds__(kNNThreads, 4)
 nn_query_kernel(TargetView T, NNQueries qs, int m, unsigned int* counter) {
     nn_packet_engine<B, false>(T, qs, m, counter);
 }
@@ -108,7 +111,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     prof_begin(kProfQuery, s);
     cudaError_t e = cudaMemsetAsync(sb, 0, 256 + b_cnt, s);
     NNQueries qs{queries, perm, std::isinf(max_dist) ? INFINITY : (float)((double)max_dist * (double)max_dist),
-                 idx, sqdist};
+                 INFINITY, idx, sqdist};
     if (e == cudaSuccess) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8));
         qcell_count_kernel<<<g, 256, 0, s>>>(t->v, queries, (int)m, qcell, cnt);

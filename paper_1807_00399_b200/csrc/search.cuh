@@ -194,10 +194,21 @@ __device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuer
 
 // work-item evaluation (any lane, for a query slot in shared memory): atomicMin on the
 // query's best key; with CERT the key that loses is pushed into the leaf-level 2nd best
-// (linearisable: every leaf minimum that is not the final one is pushed once it loses)
+// (linearisable: every leaf minimum that is not the final one is pushed once it loses), and
+// a leaf whose minimum is within the query's current threshold joins the query's candidate-
+// leaf list (capacity kListLeaves; the minimum of a leaf that does not fit is kept in drop).
+constexpr int kListLeaves = 8;
+struct CertSlots {
+    unsigned* sec;       // leaf-level 2nd best (float bits)
+    int* list;           // [kListLeaves] candidate leaves
+    int* cnt;
+    unsigned* drop;      // smallest leaf minimum that did not fit in the list (float bits)
+    const float* thr;    // the query's current threshold
+};
+
 template <int B, bool CERT>
 __device__ __forceinline__ void eval_leaf_item(const TargetView& T, const NegQuery& q, int leaf,
-                                               unsigned long long* bestS, unsigned* secS) {
+                                               unsigned long long* bestS, const CertSlots& cs) {
     float d2[B];
     leaf_d2<B>(T, q, leaf, d2);
     const float m1 = leaf_min<B>(d2);
@@ -207,7 +218,14 @@ __device__ __forceinline__ void eval_leaf_item(const TargetView& T, const NegQue
         const unsigned long long old = atomicMin(bestS, k);
         push = key_d2(old > k ? old : k);
     }
-    if (CERT && __float_as_uint(push) < *(volatile unsigned*)secS) atomicMin(secS, __float_as_uint(push));
+    if (CERT) {
+        if (__float_as_uint(push) < *(volatile unsigned*)cs.sec) atomicMin(cs.sec, __float_as_uint(push));
+        if (m1 <= *(volatile const float*)cs.thr) {
+            const int pos = atomicAdd(cs.cnt, 1);
+            if (pos < kListLeaves) cs.list[pos] = leaf;
+            else atomicMin(cs.drop, __float_as_uint(m1));
+        }
+    }
 }
 
 // Lower bound of cand_d2 over the leaf box, bit-identical to box_lb2 (the (lo, hi) pair of
@@ -269,21 +287,100 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 // than (d_out - d1) / 2.
 //
 // Q supplies
+//   __device__ int packets(int m), packet_base(int c)   (work unit c = queries base .. base+31)
 //   __device__ bool load(int i, DF3& s, unsigned long long& init, int& hint_leaf)
 //   __device__ void store(int i, unsigned long long best, float lb_out2)   (lb_out2 = 0: no certificate)
+//   CERT: store(int i, best, lb_out2, const int* list, int cnt, float rS2) with the candidate-
+//   leaf list (cnt leaves; every target outside them is at d2 >= rS2; cnt = 0: no list)
 //   float gap   (CERT only: the threshold margin g)
 constexpr int kFrontierCap = 256;
 constexpr int kItemCap = 256;
 constexpr int kDirectLeaves = 256;
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
-template <int B>
+// Independent per-lane exact DFS (nearest-child first, a subtree is entered iff its lower
+// bound is <= the lane's current threshold), for outlier lanes, overflowed packets and
+// sparse packets, whose lanes would otherwise drag each other through the union of their
+// traversals.  The hint leaf (already evaluated in phase A) is skipped.  CERT: the leaf-level
+// 2nd best and the candidate-leaf list are kept exactly as in the packet phases.
+constexpr int kDfsStack = 32;
+
+template <int B, bool CERT>
+__device__ __forceinline__ void lane_dfs(const TargetView& T, const DF3& s, const NegQuery& nq, int skip,
+                                         int skip2, float g, float cap2, unsigned long long& best, float& sec,
+                                         int* lst, int* cnt, unsigned* drop) {
+    int sv[kDfsStack];
+    float slb[kDfsStack];
+    int sp = 0;
+    int v = 1;
+    const int l_pad = T.l_pad;
+    auto thr_of = [&]() {
+        const float d = key_d2(best);
+        if (g == 0.0f) return d;
+        const float r = sqrtf(d) + g;
+        return fmaxf(fminf(r * r, cap2), d);
+    };
+    while (true) {
+        const float thr = thr_of();
+        while (v < l_pad) {
+            const int c = 2 * v;
+            const float4* bx = T.box + 2 * (size_t)c;
+            const float lb0 = box_lb2(s, __ldg(bx), __ldg(bx + 1));
+            const float lb1 = box_lb2(s, __ldg(bx + 2), __ldg(bx + 3));
+            const bool g0 = lb0 <= thr, g1 = lb1 <= thr;
+            if (g0 && g1) {
+                const bool r1 = lb1 < lb0;
+                sv[sp] = r1 ? c : c + 1;
+                slb[sp] = r1 ? lb0 : lb1;
+                ++sp;
+                v = r1 ? c + 1 : c;
+            } else if (g0) {
+                v = c;
+            } else if (g1) {
+                v = c + 1;
+            } else {
+                v = 0;
+                break;
+            }
+        }
+        if (v >= l_pad && v - l_pad != skip && v - l_pad != skip2) {
+            const int leaf = v - l_pad;
+            float d2[B];
+            leaf_d2<B>(T, nq, leaf, d2);
+            const float m1 = leaf_min<B>(d2);
+            if (CERT) {
+                sec = fminf(sec, fmaxf(key_d2(best), m1));
+                if (m1 <= thr) {
+                    if (*cnt < kListLeaves) lst[*cnt] = leaf;
+                    else *drop = min(*drop, __float_as_uint(m1));
+                    ++*cnt;
+                }
+            }
+            if (m1 <= key_d2(best)) {
+                const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
+                if (k < best) best = k;
+            }
+        }
+        v = 0;
+        while (sp > 0) {
+            --sp;
+            if (slb[sp] <= thr_of()) { v = sv[sp]; break; }
+        }
+        if (v == 0) break;
+    }
+}
+
+// Ballot DFS for the outlier lanes of a coherent packet and for packets whose frontier
+// overflowed: one traversal for the warp, a node is entered iff its lower bound is <= the
+// threshold of some searching lane (lanes that are not searching use a negative threshold).
+// Leaves are evaluated by the whole (converged) warp; only searching lanes keep the result.
+template <int B, bool CERT>
 __device__ __forceinline__ void ballot_dfs(const TargetView& T, const DF3& s, const NegQuery& nq, bool on,
-                                           float g, float cap2, unsigned long long& best) {
+                                           int skip, int skip2, float g, float cap2, unsigned long long& best, float& sec,
+                                           int* lst, int* cnt, unsigned* drop) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int l_pad = T.l_pad;
-    // lanes that are not searching use a negative threshold: no lower bound can pass it
     auto thr_of = [&]() {
         const float d = key_d2(best);
         if (!on) return -1.0f;
@@ -295,11 +392,23 @@ __device__ __forceinline__ void ballot_dfs(const TargetView& T, const DF3& s, co
     while (true) {
         const float bd = thr_of();
         if (v >= l_pad) {
-            // evaluated by the whole (converged) warp; only searching lanes keep the result
-            unsigned long long b2 = best;
-            float s2 = 0.0f;
-            eval_leaf_seq<B, false>(T, nq, v - l_pad, b2, s2);
-            if (on) best = b2;
+            const int leaf = v - l_pad;
+            float d2[B];
+            leaf_d2<B>(T, nq, leaf, d2);
+            const float m1 = leaf_min<B>(d2);
+            const uint32_t id = leaf_argmin<B>(T, leaf, d2, m1);
+            if (on && leaf != skip && leaf != skip2) {
+                if (CERT) {
+                    sec = fminf(sec, fmaxf(key_d2(best), m1));
+                    if (m1 <= bd) {
+                        if (*cnt < kListLeaves) lst[*cnt] = leaf;
+                        else *drop = min(*drop, __float_as_uint(m1));
+                        ++*cnt;
+                    }
+                }
+                const unsigned long long k = make_key(m1, id);
+                if (k < best) best = k;
+            }
         } else {
             const int c = 2 * v;
             const float4* bx = T.box + 2 * (size_t)c;
@@ -357,14 +466,21 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
     __shared__ float sQ[kEngineWarps][6][32];                 // -s_hi, -s_lo per lane
     __shared__ unsigned long long sBest[kEngineWarps][32];
     __shared__ unsigned sSec[kEngineWarps][32];
+    __shared__ int sList[CERT ? kEngineWarps : 1][32][kListLeaves];
+    __shared__ int sCnt[CERT ? kEngineWarps : 1][32];
+    __shared__ unsigned sDrop[CERT ? kEngineWarps : 1][32];
+    __shared__ float sThr[CERT ? kEngineWarps : 1][32];
     int* items = sItem[wid];
     float g = 0.0f;
     if constexpr (CERT) g = qs.gap;
+    const float stale2 = qs.stale2;                         // warm-hint distance^2 that counts as stale
+    const int npk = qs.packets(m);
     while (true) {
-        int base = 0;
-        if (lane == 0) base = (int)atomicAdd(counter, 32u);
-        base = __shfl_sync(FULL, base, 0);
-        if (base >= m) break;
+        int c = 0;
+        if (lane == 0) c = (int)atomicAdd(counter, 1u);
+        c = __shfl_sync(FULL, c, 0);
+        if (c >= npk) break;
+        const int base = qs.packet_base(c);
         const int qi = base + lane;
         const bool tracing = T.trace != nullptr;
         unsigned ck0 = tracing ? (unsigned)clock() : 0u, ckA = 0, ckB = 0, ckC = 0, ckD = 0;
@@ -372,10 +488,13 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         unsigned long long best = 0ull;
         int hint = -1;
         bool active = false;
+        bool warm = false;
         if (qi < m) {
             active = qs.load(qi, s, best, hint);
+            warm = hint >= 0;
             if (active && hint < 0) hint = coarse_hint_leaf(T, s);
         }
+        if (!__any_sync(FULL, active)) continue;                 // nothing to search in this packet
         if (!active) { s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f; best = 0ull; hint = -1; }
         const NegQuery nq = neg_query(s);
         const float cap2 = key_d2(best);                      // the search bound (rho^2 / max^2 / inf)
@@ -387,8 +506,27 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         };
         // ---- A
         float sec = INFINITY;                                 // CERT: leaf-level 2nd best
-        if (active) eval_leaf_seq<B, CERT>(T, nq, hint, best, sec);
+        int hint2 = -1;                                       // second hint leaf (cold), or -1
+        if (active) {
+            eval_leaf_seq<B, CERT>(T, nq, hint, best, sec);
+            // a warm hint that went stale (large early ICP steps): also try the leaf that
+            // follows the query's own Morton key, and keep the better of the two
+            if (warm && key_d2(best) > stale2) {
+                hint2 = coarse_hint_leaf(T, s);
+                if (hint2 != hint) eval_leaf_seq<B, CERT>(T, nq, hint2, best, sec);
+                else hint2 = -1;
+            }
+        }
         float thr = active ? thr_of(best) : 0.0f;
+        if (CERT) {
+            // the hint leaf opens the candidate list (its minimum is the current best)
+            // (a second hint leaf joins the list through its own slot)
+            sList[wid][lane][0] = hint;
+            sList[wid][lane][1] = hint2;
+            sCnt[wid][lane] = (active && best != bound_key(cap2)) ? (hint2 >= 0 ? 2 : 1) : 0;
+            sDrop[wid][lane] = __float_as_uint(INFINITY);
+            sThr[wid][lane] = thr;
+        }
         if (tracing) ckA = (unsigned)clock();
         // ---- B: outliers and the packet box
         const float r = active ? sqrtf(thr) : 0.0f;
@@ -421,10 +559,16 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             phi.y = fmaxf(phi.y, __shfl_xor_sync(FULL, phi.y, o));
             phi.z = fmaxf(phi.z, __shfl_xor_sync(FULL, phi.z, o));
         }
+        // sparse packet (the balls fill a small part of P: e.g. an uncertified remainder
+        // spread along the scan): every lane searches on its own
+        float vb = normal ? 8.0f * rx * ry * rz : 0.0f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) vb += __shfl_xor_sync(FULL, vb, o);
+        const bool sparse = (phi.x - plo.x) * (phi.y - plo.y) * (phi.z - plo.z) > 32.0f * vb;
         if (tracing) ckB = (unsigned)clock();
         bool overflow = false;
         int dbg_i0 = -1, dbg_i1 = -1, dbg_nF = -1, dbg_items = 0;
-        if (__any_sync(FULL, normal)) {
+        if (!sparse && __any_sync(FULL, normal)) {
             int* F = sF[wid][0];
             int* G = sF[wid][1];
             // ---- C: Morton range of P -> leaf range -> candidate leaves (node ids)
@@ -498,7 +642,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                 for (int k = 0; k < nF; ++k) {
                     const int f = F[k];
                     const float lb = leaf_lb2(T, nq, f);
-                    const bool need = normal && f != hint && lb <= thr;
+                    const bool need = normal && f != hint && f != hint2 && lb <= thr;
                     const unsigned mk = __ballot_sync(FULL, need);
                     if (need) items[nI + __popc(mk & lt)] = (f << 5) | lane;
                     nI += __popc(mk);
@@ -517,7 +661,12 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                                 qq.lx = make_float2(sQ[wid][3][q], sQ[wid][3][q]);
                                 qq.ly = make_float2(sQ[wid][4][q], sQ[wid][4][q]);
                                 qq.lz = make_float2(sQ[wid][5][q], sQ[wid][5][q]);
-                                eval_leaf_item<B, CERT>(T, qq, it >> 5, &sBest[wid][q], &sSec[wid][q]);
+                                CertSlots cs;
+                                if (CERT) {
+                                    cs.sec = &sSec[wid][q]; cs.list = sList[wid][q]; cs.cnt = &sCnt[wid][q];
+                                    cs.drop = &sDrop[wid][q]; cs.thr = &sThr[wid][q];
+                                }
+                                eval_leaf_item<B, CERT>(T, qq, it >> 5, &sBest[wid][q], cs);
                             }
                         }
                         __syncwarp();
@@ -525,6 +674,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                         best = sBest[wid][lane];
                         if (CERT) sec = __uint_as_float(sSec[wid][lane]);
                         if (active) thr = thr_of(best);
+                        if (CERT) sThr[wid][lane] = thr;
                     }
                 }
             }
@@ -533,7 +683,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         int* trace = T.trace;
         if (trace && qi < m) {
             int* rec = trace + 16 * (size_t)qi;
-            rec[0] = normal | (outlier << 1) | (overflow << 2);
+            rec[0] = normal | (outlier << 1) | (overflow << 2) | (sparse << 3);
             rec[1] = __float_as_int(r);
             rec[2] = dbg_i0; rec[3] = dbg_i1; rec[4] = dbg_nF;
             rec[5] = __float_as_int(key_d2(best));
@@ -541,16 +691,36 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             rec[8] = (int)(ckA - ck0); rec[9] = (int)(ckB - ckA); rec[10] = (int)(ckC - ckB); rec[11] = (int)(ckD - ckC);
         }
         // ---- F: exact ballot DFS for outliers (or everyone after an overflow)
-        const bool dfs_on = outlier || (overflow && normal);
-        if (__any_sync(FULL, dfs_on)) ballot_dfs<B>(T, s, nq, dfs_on, g, cap2, best);
+        // sparse packet: independent per-lane DFS; outliers / overflow: ballot DFS
+        const bool lane_on = sparse && normal;
+        const bool ballot_on = outlier || (overflow && normal);
+        {
+            unsigned drop = 0u;
+            int cnt = 0;
+            int* lst = nullptr;
+            if constexpr (CERT) { drop = sDrop[wid][lane]; cnt = sCnt[wid][lane]; lst = sList[wid][lane]; }
+            if (lane_on) lane_dfs<B, CERT>(T, s, nq, hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
+            if (__any_sync(FULL, ballot_on))
+                ballot_dfs<B, CERT>(T, s, nq, ballot_on, hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
+            if constexpr (CERT) { sDrop[wid][lane] = drop; sCnt[wid][lane] = cnt; }
+            if (active && (lane_on || ballot_on)) thr = thr_of(best);
+        }
         if (trace && qi < m) {
             trace[16 * (size_t)qi + 7] = __float_as_int(key_d2(best));
             trace[16 * (size_t)qi + 12] = (int)((unsigned)clock() - ckD);
         }
         if (active) {
             // targets outside the evaluated leaves are beyond the final threshold
-            const float lb_out2 = (CERT && normal && !overflow) ? fminf(sec, thr) : 0.0f;
-            qs.store(qi, best, lb_out2);
+            const bool cert_ok = CERT;
+            const float lb_out2 = cert_ok ? fminf(sec, thr) : 0.0f;
+            if constexpr (CERT) {
+                // candidate-leaf list: every target outside it is beyond min(thr, drop)
+                const int cnt = cert_ok ? min(sCnt[wid][lane], kListLeaves) : 0;
+                const float rS2 = fminf(thr, __uint_as_float(sDrop[wid][lane]));
+                qs.store(qi, best, lb_out2, sList[wid][lane], cnt, rS2);
+            } else {
+                qs.store(qi, best, lb_out2);
+            }
         }
         __syncwarp();
     }

@@ -54,3 +54,19 @@ for k in (2, 10, 30):
     torch.cuda.synchronize()
     cil.lib().cil_debug_engine_trace(None)
     summarize(f"run (no cert) iteration {k}", tr.cpu().numpy().reshape(-1, 16))
+
+cil.set_certificates(True)
+for k in (40,):
+    pk = cil.make_params(metric, k, 1.0)
+    ws = cil.alloc_workspace(w.m, pk)
+    tr[:] = 0
+    cil.lib().cil_debug_engine_trace(tr.data_ptr())
+    cil.cil_icp_run(t, src, d(np.eye(4)), pk, ws=ws)
+    torch.cuda.synchronize()
+    cil.lib().cil_debug_engine_trace(None)
+    a = tr.cpu().numpy().reshape(-1, 16)
+    n_last = int((a[:, 8] != 0).sum())   # slots of the last (smallest) list are overwritten last
+    print("cert run: slots with a trace record", n_last, "(records of the last iterations overlap)")
+    fl = a[:, 0]
+    print("  flags: normal", int((fl & 1).sum()), "outlier", int(((fl >> 1) & 1).sum()), "overflow", int(((fl >> 2) & 1).sum()),
+          "sparse", int(((fl >> 3) & 1).sum()))

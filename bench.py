@@ -221,7 +221,8 @@ def run_ours(args, rank, world, local_rank):
             "icp_select_kernel_ms": sel_ms, "icp_nn_kernel_ms": nn_ms, "icp_acc_kernel_ms": acc_ms,
             "run_ms": run_ms / args.steps,
             "full_searches_per_run": cil.run_searched(ws) / w.m,
-            "timed_launches": {"nn": prof["n_nn"], "acc": prof["n_acc"], "build": prof["n_build"]},
+            "timed_launches": {"select": prof["n_sel"], "nn": prof["n_nn"], "acc": prof["n_acc"],
+                               "build": prof["n_build"]},
             "final_status": r.status, "final_n_corr": r.n_corr, "final_rmse": r.rmse,
             "parallelism": f"independent frame pair per rank x{world}",
         },
@@ -245,11 +246,13 @@ def C_sizeof(ct):
 
 
 def _traffic_from_profiles(workload):
-    """dram bytes per icp_iter_kernel launch from the committed ncu --set full summary"""
+    """dram bytes of one steady-state ICP iteration (select + nn + acc kernels) from the committed
+    ncu --set full captures (profiles/traffic.json)"""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(workload)
+            t = json.load(f).get(workload)
+        return None if t is None else t.get("steady_iteration_bytes")
     except Exception:
         return None
 

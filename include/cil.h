@@ -216,10 +216,13 @@ cil_status cil_profile_read(cil_profile_stats* out);
    warm start); used to measure the certificate.  Host-only, process-wide. */
 cil_status cil_debug_set_flags(uint32_t flags);
 
-/* Tuning: margin g of the leaf certificate of cil_icp_run as a fraction of max_corr_dist
-   (default 0.002): K_nn searches to (sqrt(best) + g)^2 so that a match is certified to stay
-   in its leaf while the point moves less than about g/2.  0 <= frac <= 1.  Host-only. */
-cil_status cil_debug_set_cert_gap(double frac);
+/* Tuning: the certificate skin of cil_icp_run.  A full search of point p uses the threshold
+   (sqrt(best) + g)^2 with g = clamp(kappa * (p's displacement in the last iteration),
+   min_frac * max_corr_dist, max_frac * max_corr_dist), so that its match is certified (leaf /
+   candidate list) while p moves less than about g / 2 (a point moving faster than
+   4 max_frac * max_corr_dist / kappa per iteration uses the minimum).  Defaults 0.001, 0.005, 16.
+   0 <= min_frac <= max_frac <= 1, kappa >= 0.  Host-only, process-wide. */
+cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kappa);
 
 /* Diagnostics: while buf (device int32, >= 16 per query slot) is non-NULL, every search-engine
    launch writes per processed query slot {flags, r, i0, i1, nF, best d2 after the packet

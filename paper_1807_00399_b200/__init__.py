@@ -44,7 +44,7 @@ METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_
 EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
             "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
-            "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_gap"]
+            "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin"]
 
 
 class cil_index_params(C.Structure):
@@ -108,8 +108,8 @@ _lib.cil_debug_set_flags.restype = C.c_int
 _lib.cil_debug_set_flags.argtypes = [C.c_uint32]
 _lib.cil_debug_engine_trace.restype = C.c_int
 _lib.cil_debug_engine_trace.argtypes = [C.c_void_p]
-_lib.cil_debug_set_cert_gap.restype = C.c_int
-_lib.cil_debug_set_cert_gap.argtypes = [C.c_double]
+_lib.cil_debug_set_cert_skin.restype = C.c_int
+_lib.cil_debug_set_cert_skin.argtypes = [C.c_double, C.c_double, C.c_double]
 
 # Byte offsets into the ICP workspace (csrc/icp.cu ws_layout, IcpState) -- diagnostics only.
 WS_STATE_SEARCHED = 176       # int64: sum over executed iterations of the search-list size
@@ -120,9 +120,9 @@ def set_certificates(on: bool = True) -> None:
     _check(_lib.cil_debug_set_flags(0 if on else 1), "cil_debug_set_flags")
 
 
-def set_cert_gap(frac: float) -> None:
-    """leaf-certificate margin g / max_corr_dist of cil_icp_run (tuning; default 0.01)"""
-    _check(_lib.cil_debug_set_cert_gap(float(frac)), "cil_debug_set_cert_gap")
+def set_cert_skin(min_frac: float = 0.001, max_frac: float = 0.005, kappa: float = 16.0) -> None:
+    """certificate skin of cil_icp_run: g = clamp(kappa * last-step displacement, min, max) x max_corr_dist"""
+    _check(_lib.cil_debug_set_cert_skin(float(min_frac), float(max_frac), float(kappa)), "cil_debug_set_cert_skin")
 
 
 def run_searched(ws: torch.Tensor) -> int:

@@ -24,9 +24,13 @@ int* g_trace = nullptr;
 }
 int* debug_trace() { return g_trace; }
 namespace {
-double g_cert_gap = 0.002;
+double g_skin_min = 0.001, g_skin_max = 0.005, g_skin_kappa = 16.0;
 }
-double cert_gap_frac() { return g_cert_gap; }
+void cert_skin_params(double* gmin, double* gmax, double* kappa) {
+    *gmin = g_skin_min;
+    *gmax = g_skin_max;
+    *kappa = g_skin_kappa;
+}
 void set_debug_trace(int* p) { g_trace = p; }
 
 namespace {
@@ -145,9 +149,11 @@ CIL_API cil_status cil_profile_read(cil_profile_stats* out) {
     return CIL_OK;
 }
 
-CIL_API cil_status cil_debug_set_cert_gap(double frac) {
-    if (!(frac >= 0.0) || frac > 1.0) return CIL_ERR_INVALID_ARG;
-    cil::g_cert_gap = frac;
+CIL_API cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kappa) {
+    if (!(min_frac >= 0.0) || !(max_frac >= min_frac) || max_frac > 1.0 || !(kappa >= 0.0)) return CIL_ERR_INVALID_ARG;
+    cil::g_skin_min = min_frac;
+    cil::g_skin_max = max_frac;
+    cil::g_skin_kappa = kappa;
     return CIL_OK;
 }
 

@@ -45,7 +45,7 @@ struct IterArgs {
     float bound2;            // fl32(max_corr_dist^2): acceptance (a3)
     float search2;           // search bound: bound2, or fl32(rho^2) with certificates
     float gap_none;          // certificate of "no target within rho": rho - max_corr_dist (rounded down)
-    float cert_gap;          // search-threshold margin g of the leaf certificate
+    float gap_min, gap_max, kappa;   // per-point certificate skin clamp(kappa * last step, gap_min, gap_max)
     float stale2;            // (max_corr_dist / 10)^2: a warm hint beyond it is stale
     const double* pose_in;
     double* pose_out;
@@ -57,6 +57,8 @@ struct IterArgs {
     int* nn;                 // [m] match per query (original target index or -1)
     uint32_t* gw;            // [m] leaf-certificate word (run): bits(G1) & ~255 | anchor slot
     float* gs;               // [m] list-certificate margin G_S (run)
+    float* gd1;              // [m] d1 at the search anchor, rounded up (run)
+    uint32_t* gp;            // [m] point certificate: bits(G_pt) & ~255 | slot of the iteration it was measured
     int* vlist;              // [m][kListLeaves] candidate leaves of the last search (run), -1 padded
     uint32_t* pmask;         // [ceil(m/32)] per 32-query packet: lanes that need a full search (run)
     int* plist;              // [ceil(m/32)] packets with a non-empty mask (any order; count st->plist_n)
@@ -65,6 +67,7 @@ struct IterArgs {
     double* iter_log;        // run only, nullable
     int run;
     int cert;                // run: certified warm start on
+    int point_cert;          // run: the point-level certificate on (diagnostics switch)
     double rot_tol, trans_tol;
 };
 
@@ -247,19 +250,41 @@ constexpr int kSelTile = kSelThreads * kSelRounds;     // 512 queries per CTA
 
 // Certificates of query i at the current pose, one query per lane, the
 // whole warp together: returns true if the lane's query needs a full search; otherwise its
-// exact nearest neighbour is found here and written to nn[i]:
-//   leaf certificate  G1 > 2 D : the NN is in the previous match's leaf L1;
+// exact nearest neighbour is known after this call (nn[i]):
+//   point certificate G_pt > 2 D_p: the match j1 itself is unchanged (no evaluation at all);
+//     G_pt is re-measured whenever the leaf / list is evaluated (anchor = that iteration);
+//   leaf certificate  G1 > 2 D : the NN is in the search anchor's leaf L1 (one leaf evaluated);
 //   list certificate  G_S > 2 D: the NN is in the stored candidate-leaf list (a Verlet list
 //                                with skin g: every other target was beyond r_S = d1 + G_S);
 //   nothing within rho, G1 = rho - max_corr_dist > D: still nothing within max_corr_dist.
-// The (query, leaf) evaluations of the warp are flattened into rounds of 32 independent
-// items (shared-memory atomicMin on the queries' u64 keys), so a warp keeps 32 leaf loads
-// in flight instead of walking each lane's list in sequence.
+// Evaluations are flattened over the warp into rounds of 32 independent (query, leaf) items
+// (shared-memory atomicMin on u64 keys), so a warp keeps 32 leaf loads in flight.
 struct SelWarp {
     float q[6][32];                          // -s_hi, -s_lo per lane
     unsigned long long best[32];
+    unsigned sec[32];                        // point-level 2nd best (float bits)
     int items[32 * kListLeaves];
 };
+
+// leaf item for K_sel: best key and the point-level second best (the loser of every merge and
+// the within-leaf second minimum)
+template <int B>
+__device__ __forceinline__ void sel_leaf_item(const TargetView& T, const NegQuery& q, int leaf,
+                                              unsigned long long* bestS, unsigned* secS) {
+    float d2[B];
+    leaf_d2<B>(T, q, leaf, d2);
+    float m1 = d2[0], m2 = INFINITY;
+#pragma unroll
+    for (int c = 1; c < B; ++c) { m2 = fminf(m2, fmaxf(m1, d2[c])); m1 = fminf(m1, d2[c]); }
+    float push = m1;
+    if (m1 <= key_d2(*(volatile unsigned long long*)bestS)) {
+        const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
+        const unsigned long long old = atomicMin(bestS, k);
+        push = old == k ? INFINITY : key_d2(old > k ? old : k);
+    }
+    const unsigned v = __float_as_uint(fminf(push, m2));
+    if (v < *(volatile unsigned*)secS) atomicMin(secS, v);
+}
 
 template <int B>
 __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P, int i, uint32_t kslot, SelWarp& S) {
@@ -267,14 +292,17 @@ __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P,
     const int lane = threadIdx.x & 31;
     bool need = false;
     int nit = 0, j = -1;
+    float outer = 0.0f;                      // lower bound of |s' - t| for every t outside the evaluated leaves
     int4 l0 = make_int4(-1, -1, -1, -1), l1 = make_int4(-1, -1, -1, -1);
     if (i < a.m) {
         const uint32_t w = a.gw[i];
+        const uint32_t wp = a.gp[i];
+        const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
+        const float Gp = __uint_as_float(wp & ~255u);
         // slot == kslot: never anchored (iteration 0) or an anchor pose being recycled (k >= 256)
         if ((w & 255u) == kslot) {
             need = true;
         } else {
-            const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
             const float D = displacement_bound(a.adelta + 16 * (w & 255u), px, py, pz);
             const float G1 = __uint_as_float(w & ~255u);
             j = a.nn[i];
@@ -282,33 +310,40 @@ __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P,
                 need = !(G1 > D);
             } else {
                 const bool leaf_ok = G1 > 2.0f * D;
-                if (leaf_ok || a.gs[i] > 2.0f * D) {
+                const float GS = leaf_ok ? 0.0f : a.gs[i];
+                if (!leaf_ok && !(GS > 2.0f * D)) {
+                    need = true;
+                } else if (a.point_cert && (wp & 255u) != kslot && Gp > 0.0f &&
+                           Gp > 2.0f * displacement_bound(a.adelta + 16 * (wp & 255u), px, py, pz)) {
+                    // point certificate (only where the leaf / list certificate holds too, so it
+                    // never postpones a search): nn[i] stays, nothing to evaluate
+                } else {
                     const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
                     l0 = vl[0];
                     if (!leaf_ok) l1 = vl[1];
                     nit = leaf_ok ? 1
                                   : (l0.x >= 0) + (l0.y >= 0) + (l0.z >= 0) + (l0.w >= 0) + (l1.x >= 0) +
                                         (l1.y >= 0) + (l1.z >= 0) + (l1.w >= 0);
+                    // targets outside the evaluated leaves were >= d_out (resp. r_S) from the anchor
+                    outer = (leaf_ok ? G1 : GS) + a.gd1[i] - D;
                     const DF3 s = transform_df(P, px, py, pz);
                     S.q[0][lane] = -s.hx; S.q[1][lane] = -s.hy; S.q[2][lane] = -s.hz;
                     S.q[3][lane] = -s.lx; S.q[4][lane] = -s.ly; S.q[5][lane] = -s.lz;
                     S.best[lane] = bound_key(INFINITY);
-                } else {
-                    need = true;
+                    S.sec[lane] = __float_as_uint(INFINITY);
                 }
             }
         }
     }
-    // phase 1: L1 (the anchor match's leaf, entry 0) of every certified lane -- usually the
-    // winner; phase 2: the rest of the lists, flattened into rounds of 32 (query, leaf) items,
-    // each evaluated only if the leaf box can still beat the query's current best
-    const CertSlots none{};
+    // phase 1: L1 (entry 0) of every evaluating lane -- usually the winner; phase 2: the rest of
+    // the lists, flattened into rounds of 32 (query, leaf) items, each evaluated only if the
+    // leaf box can still beat the query's current best (else its bound joins the 2nd best)
     NegQuery nq0;
     if (nit > 0) {
         nq0.hx = make_float2(S.q[0][lane], S.q[0][lane]); nq0.hy = make_float2(S.q[1][lane], S.q[1][lane]);
         nq0.hz = make_float2(S.q[2][lane], S.q[2][lane]); nq0.lx = make_float2(S.q[3][lane], S.q[3][lane]);
         nq0.ly = make_float2(S.q[4][lane], S.q[4][lane]); nq0.lz = make_float2(S.q[5][lane], S.q[5][lane]);
-        eval_leaf_item<B, false>(a.T, nq0, l0.x, &S.best[lane], none);
+        sel_leaf_item<B>(a.T, nq0, l0.x, &S.best[lane], &S.sec[lane]);
     }
     const int rest = nit > 1 ? nit - 1 : 0;
     int incl = rest;
@@ -318,32 +353,40 @@ __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P,
         if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(FULL, incl, 31);
-    const int excl = incl - rest;
-    const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    if (total > 0) {
+        const int excl = incl - rest;
+        const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-    for (int c = 1; c < kListLeaves; ++c)
-        if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
-    __syncwarp();
-    for (int r0 = 0; r0 < total; r0 += 32) {
-        const int k = r0 + lane;
-        if (k < total) {
-            const int it = S.items[k];
-            const int q = it & 31;
-            NegQuery qq;
-            qq.hx = make_float2(S.q[0][q], S.q[0][q]);
-            qq.hy = make_float2(S.q[1][q], S.q[1][q]);
-            qq.hz = make_float2(S.q[2][q], S.q[2][q]);
-            qq.lx = make_float2(S.q[3][q], S.q[3][q]);
-            qq.ly = make_float2(S.q[4][q], S.q[4][q]);
-            qq.lz = make_float2(S.q[5][q], S.q[5][q]);
-            if (leaf_lb2(a.T, qq, it >> 5) <= key_d2(*(volatile unsigned long long*)&S.best[q]))
-                eval_leaf_item<B, false>(a.T, qq, it >> 5, &S.best[q], none);
+        for (int c = 1; c < kListLeaves; ++c)
+            if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
+        __syncwarp();
+        for (int r0 = 0; r0 < total; r0 += 32) {
+            const int k = r0 + lane;
+            if (k < total) {
+                const int it = S.items[k];
+                const int q = it & 31;
+                NegQuery qq;
+                qq.hx = make_float2(S.q[0][q], S.q[0][q]);
+                qq.hy = make_float2(S.q[1][q], S.q[1][q]);
+                qq.hz = make_float2(S.q[2][q], S.q[2][q]);
+                qq.lx = make_float2(S.q[3][q], S.q[3][q]);
+                qq.ly = make_float2(S.q[4][q], S.q[4][q]);
+                qq.lz = make_float2(S.q[5][q], S.q[5][q]);
+                const float lb = leaf_lb2(a.T, qq, it >> 5);
+                if (lb <= key_d2(*(volatile unsigned long long*)&S.best[q])) sel_leaf_item<B>(a.T, qq, it >> 5, &S.best[q], &S.sec[q]);
+                else atomicMin(&S.sec[q], __float_as_uint(lb));
+            }
         }
     }
     __syncwarp();
     if (nit > 0) {
-        const int jn = (int)key_idx(S.best[lane]);
+        const unsigned long long b = S.best[lane];
+        const int jn = (int)key_idx(b);
         if (jn != j) a.nn[i] = jn;
+        // point certificate measured here: every other target is at >= min(2nd best, outer)
+        const float o2 = fminf(sqrtf(__uint_as_float(S.sec[lane])), outer);
+        const float Gp = fmaxf(o2 * (1.0f - 4e-6f) - sqrtf(key_d2(b)) * (1.0f + 4e-6f), 0.0f);
+        a.gp[i] = (__float_as_uint(Gp) & ~255u) | kslot;
     }
     __syncwarp();
     return need;
@@ -401,11 +444,16 @@ struct IcpQueries {
     Pose34 P;
     float search2;
     float gap_none;
-    float gap;               // CERT: search-threshold margin g (leaf form)
+    float gap_min, gap_max;  // CERT: the skin g of a point = clamp(kappa x its last-step displacement)
+    float kappa;
+    const float* prev_delta; // anchor-table entry of the previous iteration (pose_k - pose_{k-1}) or nullptr
+    mutable float skin;      // out of load(): this query's skin
     float stale2;            // a warm hint farther than this (d^2) is complemented by the cold hint
     int* nn;
     uint32_t* gw;
     float* gs;
+    float* gd1;
+    uint32_t* gp;
     int* vlist;
     const uint32_t* pmask;
     const int* plist;        // CERT: packets with a non-empty mask, count at *plist_n
@@ -418,8 +466,21 @@ struct IcpQueries {
     __device__ __forceinline__ int packet_base(int c) const { return 32 * (plist ? plist[c] : c); }
     __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
         if (pmask && !((pmask[i >> 5] >> (i & 31)) & 1u)) return false;    // certified in K_sel
-        s = transform_df(P, src[3 * (size_t)i], src[3 * (size_t)i + 1], src[3 * (size_t)i + 2]);
+        const float px = src[3 * (size_t)i], py = src[3 * (size_t)i + 1], pz = src[3 * (size_t)i + 2];
+        s = transform_df(P, px, py, pz);
         init = bound_key(search2);
+        if (CERT) {
+            // per-point skin: a multiple of the point's own displacement in the last iteration
+            // (the certificate then tends to hold for the next several, geometrically shrinking steps)
+            // (a point moving faster than 4 gap_max / kappa per iteration would not keep a
+            // certificate anyway: it searches with the minimal skin, the cheapest search)
+            float sk = gap_min;
+            if (prev_delta) {
+                const float want = kappa * displacement_bound(prev_delta, px, py, pz);
+                sk = want <= 4.0f * gap_max ? fminf(fmaxf(want, gap_min), gap_max) : gap_min;
+            }
+            skin = sk;
+        }
         const int j = warm ? nn[i] : -1;
         hint = j >= 0 ? __float_as_int(__ldg(&opts[j].w)) / B : -1;
         return true;
@@ -445,6 +506,8 @@ struct IcpQueries {
         }
         gw[i] = (__float_as_uint(G1) & ~255u) | slot;
         gs[i] = GS;
+        gd1[i] = found ? sqrtf(key_d2(best)) * (1.0f + 4e-6f) : 0.0f;
+        gp[i] = slot;                        // no point certificate yet (G_pt = 0)
         // entry 0 = L1, the anchor match's leaf (the leaf certificate refers to it even after a
         // list-certified iteration moved the match to another leaf), then the rest of the list
         const int L1 = found ? __float_as_int(__ldg(&opts[key_idx(best)].w)) / B : -1;
@@ -480,11 +543,20 @@ icp_nn_kernel(const IterArgs a) {
     for (int k = 0; k < 12; ++k) qs.P.r[k] = __ldg(a.pose_in + k);
     qs.search2 = a.search2;
     qs.gap_none = a.gap_none;
-    qs.gap = a.cert_gap;
+    qs.gap_min = a.gap_min;
+    qs.gap_max = a.gap_max;
+    qs.kappa = a.kappa;
+    {
+        const int k = a.run ? *(volatile int*)&a.st->iters : 0;
+        qs.prev_delta = (a.cert && k > 0) ? a.adelta + 16 * ((k - 1) & (kAnchorSlots - 1)) : nullptr;
+    }
+    qs.skin = 0.0f;
     qs.stale2 = a.stale2;
     qs.nn = a.nn;
     qs.gw = a.gw;
     qs.gs = a.gs;
+    qs.gd1 = a.gd1;
+    qs.gp = a.gp;
     qs.vlist = a.vlist;
     qs.pmask = a.cert ? a.pmask : nullptr;
     qs.plist = a.cert ? a.plist : nullptr;
@@ -494,6 +566,43 @@ icp_nn_kernel(const IterArgs a) {
     qs.corr_idx = a.corr_idx;
     qs.corr_d2 = a.corr_d2;
     nn_packet_engine<B, CERT>(a.T, qs, a.m, &a.st->work);
+}
+
+// a1 + a3 + a4 + a5 for the pair (p, t): transform, inclusive rejection (R2), residual,
+// Jacobian, fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
+template <int METRIC>
+__device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose34& P, float px, float py, float pz,
+                                                float4 t, float4 n, float bound2) {
+    const DF3 s = transform_df(P, px, py, pz);
+    const float dx = dfdiff(s.hx, s.lx, t.x);
+    const float dy = dfdiff(s.hy, s.ly, t.y);
+    const float dz = dfdiff(s.hz, s.lz, t.z);
+    if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= bound2)) return;
+    if (METRIC == CIL_POINT_TO_PLANE) {
+        const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
+        const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
+                            fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
+        int k = 0;
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+            for (int q = p; q < 6; ++q, ++k) acc[k] = fmaf(J[p], J[q], acc[k]);
+#pragma unroll
+        for (int p = 0; p < 6; ++p) acc[21 + p] = fmaf(J[p], r, acc[21 + p]);
+        acc[27] = fmaf(r, r, acc[27]);
+        acc[28] += 1.0f;
+    } else {
+        const float sx = s.hx, sy = s.hy, sz = s.hz;
+        acc[0] += 1.0f;
+        acc[1] += sx; acc[2] += sy; acc[3] += sz;
+        acc[4] = fmaf(sx, sx, acc[4]); acc[5] = fmaf(sy, sy, acc[5]); acc[6] = fmaf(sz, sz, acc[6]);
+        acc[7] = fmaf(sx, sy, acc[7]); acc[8] = fmaf(sx, sz, acc[8]); acc[9] = fmaf(sy, sz, acc[9]);
+        acc[10] += dx; acc[11] += dy; acc[12] += dz;
+        acc[13] += fmaf(sy, dz, -sz * dy);
+        acc[14] += fmaf(sz, dx, -sx * dz);
+        acc[15] += fmaf(sx, dy, -sy * dx);
+        acc[16] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, acc[16])));
+    }
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
@@ -517,40 +626,6 @@ icp_acc_kernel(const IterArgs a) {
     for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
 
     const TargetView& T = a.T;
-    // a1 + a3 + a4 + a5 for the pair (p, t_j): transform, inclusive rejection (R2), residual,
-    // Jacobian, fp32 per-thread sums
-    auto pair = [&](float px, float py, float pz, float4 t, float4 n) {
-        const DF3 s = transform_df(P, px, py, pz);
-        const float dx = dfdiff(s.hx, s.lx, t.x);
-        const float dy = dfdiff(s.hy, s.ly, t.y);
-        const float dz = dfdiff(s.hz, s.lz, t.z);
-        if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= a.bound2)) return;
-        if (METRIC == CIL_POINT_TO_PLANE) {
-            const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
-            const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
-                                fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
-            int k = 0;
-#pragma unroll
-            for (int p = 0; p < 6; ++p)
-#pragma unroll
-                for (int q = p; q < 6; ++q, ++k) acc[k] = fmaf(J[p], J[q], acc[k]);
-#pragma unroll
-            for (int p = 0; p < 6; ++p) acc[21 + p] = fmaf(J[p], r, acc[21 + p]);
-            acc[27] = fmaf(r, r, acc[27]);
-            acc[28] += 1.0f;
-        } else {
-            const float sx = s.hx, sy = s.hy, sz = s.hz;
-            acc[0] += 1.0f;
-            acc[1] += sx; acc[2] += sy; acc[3] += sz;
-            acc[4] = fmaf(sx, sx, acc[4]); acc[5] = fmaf(sy, sy, acc[5]); acc[6] = fmaf(sz, sz, acc[6]);
-            acc[7] = fmaf(sx, sy, acc[7]); acc[8] = fmaf(sx, sz, acc[8]); acc[9] = fmaf(sy, sz, acc[9]);
-            acc[10] += dx; acc[11] += dy; acc[12] += dz;
-            acc[13] += fmaf(sy, dz, -sz * dy);
-            acc[14] += fmaf(sz, dx, -sx * dz);
-            acc[15] += fmaf(sx, dy, -sy * dx);
-            acc[16] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, acc[16])));
-        }
-    };
     // two queries per trip with every load issued before the arithmetic (the gathers depend on
     // nn[]; two independent chains in flight per thread); summation order = grid-stride order
     const int stride = gridDim.x * blockDim.x;
@@ -571,8 +646,8 @@ icp_acc_kernel(const IterArgs a) {
             if (METRIC == CIL_POINT_TO_PLANE) n1 = __ldg(T.onrm + j1);
             p1x = a.src[3 * (size_t)i1]; p1y = a.src[3 * (size_t)i1 + 1]; p1z = a.src[3 * (size_t)i1 + 2];
         }
-        if (j0 >= 0) pair(p0x, p0y, p0z, t0, n0);                       // a3: j < 0 = nothing within the bound
-        if (j1 >= 0) pair(p1x, p1y, p1z, t1, n1);
+        if (j0 >= 0) accumulate_pair<METRIC>(acc, P, p0x, p0y, p0z, t0, n0, a.bound2);   // a3: j < 0 = rejected
+        if (j1 >= 0) accumulate_pair<METRIC>(acc, P, p1x, p1y, p1z, t1, n1, a.bound2);
     }
 
     // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
@@ -647,7 +722,7 @@ icp_acc_kernel(const IterArgs a) {
 }
 
 // ---------------------------------------------------------------- run bookkeeping kernels
-__global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, uint32_t* gw, int m,
+__global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, uint32_t* gw, uint32_t* gp, int m,
                                 double* iter_log, int log_len) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0) {
@@ -655,7 +730,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, 
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
         st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
     }
-    for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; }
+    for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; gp[i] = 0u; }
     if (iter_log)
         for (int i = tid; i < log_len; i += gridDim.x * blockDim.x) iter_log[i] = 0.0;
 }
@@ -742,7 +817,7 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
 }
 
 struct WsLayout {
-    size_t state, partials, apose, adelta, nn, gw, pmask, plist, gs, vlist, total;
+    size_t state, partials, apose, adelta, nn, gw, pmask, plist, gs, gd1, gp, vlist, total;
 };
 
 WsLayout ws_layout(int64_t m) {
@@ -757,7 +832,9 @@ WsLayout ws_layout(int64_t m) {
     L.pmask = L.gw + align_up(mm * sizeof(uint32_t), 256);
     L.plist = L.pmask + align_up((mm + 31) / 32 * sizeof(uint32_t), 256);
     L.gs = L.plist + align_up((mm + 31) / 32 * sizeof(int), 256);
-    L.vlist = L.gs + align_up(mm * sizeof(float), 256);
+    L.gd1 = L.gs + align_up(mm * sizeof(float), 256);
+    L.gp = L.gd1 + align_up(mm * sizeof(float), 256);
+    L.vlist = L.gp + align_up(mm * sizeof(uint32_t), 256);
     L.total = L.vlist + align_up(mm * kListLeaves * sizeof(int), 256);
     return L;
 }
@@ -774,6 +851,8 @@ void bind_ws(IterArgs& a, void* ws, int64_t m) {
     a.pmask = (uint32_t*)(w + L.pmask);
     a.plist = (int*)(w + L.plist);
     a.gs = (float*)(w + L.gs);
+    a.gd1 = (float*)(w + L.gd1);
+    a.gp = (uint32_t*)(w + L.gp);
     a.vlist = (int*)(w + L.vlist);
 }
 
@@ -858,6 +937,7 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.m = (int)m;
     a.bound2 = bound2_of(params->max_corr_dist);
     a.cert = (debug_flags() & 1u) ? 0 : 1;
+    a.point_cert = (debug_flags() & 8u) ? 0 : 1;
     // certificates search to rho = 1.1 max_corr_dist so that a point with
     // nothing within rho stays provably rejected while it moves less than rho - max_corr_dist
     const double rho = std::isinf(params->max_corr_dist) ? INFINITY : 1.1 * params->max_corr_dist;
@@ -869,7 +949,14 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
         a.gap_none = g;
     }
     // leaf-certificate margin g: the search threshold of K_nn is (sqrt(best) + g)^2
-    a.cert_gap = (float)(cert_gap_frac() * (std::isinf(params->max_corr_dist) ? 0.0 : params->max_corr_dist));
+    {
+        double gmin = 0.0, gmax = 0.0, kap = 0.0;
+        cert_skin_params(&gmin, &gmax, &kap);
+        const double md = std::isinf(params->max_corr_dist) ? 0.0 : params->max_corr_dist;
+        a.gap_min = (float)(gmin * md);
+        a.gap_max = (float)(gmax * md);
+        a.kappa = (float)kap;
+    }
     a.stale2 = std::isinf(params->max_corr_dist) ? INFINITY : (float)(0.01 * params->max_corr_dist * params->max_corr_dist);
     a.pose_in = a.st->pose;
     a.pose_out = a.st->pose;
@@ -879,7 +966,7 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.trans_tol = params->trans_tol;
     cudaStream_t s = (cudaStream_t)stream;
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
-    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, (int)m, iter_log,
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, a.gp, (int)m, iter_log,
                                                 2 * params->max_iters);
     count_launches(1);
     cudaError_t e = cudaGetLastError();

@@ -81,7 +81,7 @@ cudaError_t pool_free(void* p, cudaStream_t s);
 void count_launches(int k);   // diagnostics counter behind cil_launch_count()
 unsigned debug_flags();       // cil_debug_set_flags (bit 0: no certified warm start)
 int* debug_trace();           // cil_debug_engine_trace buffer (nullptr = off)
-double cert_gap_frac();       // leaf-certificate margin g / max_corr_dist (cil_debug_set_cert_gap)
+void cert_skin_params(double* gmin, double* gmax, double* kappa);   // cil_debug_set_cert_skin
 void set_debug_trace(int* p);
 
 // diagnostics: per-launch event timing (cil_profile_*)

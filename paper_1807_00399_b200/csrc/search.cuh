@@ -185,10 +185,13 @@ __device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuer
     float d2[B];
     leaf_d2<B>(T, q, leaf, d2);
     const float m1 = leaf_min<B>(d2);
-    if (CERT) sec = fminf(sec, fmaxf(key_d2(best), m1));
     if (m1 <= key_d2(best)) {
         const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
+        // (k == best: the same point was already offered, e.g. by a neighbour lane -- not a loser)
+        if (CERT && k != best) sec = fminf(sec, fmaxf(key_d2(best), m1));
         if (k < best) best = k;
+    } else if (CERT) {
+        sec = fminf(sec, m1);
     }
 }
 
@@ -216,7 +219,7 @@ __device__ __forceinline__ void eval_leaf_item(const TargetView& T, const NegQue
     if (m1 <= key_d2(*(volatile unsigned long long*)bestS)) {
         const unsigned long long k = make_key(m1, leaf_argmin<B>(T, leaf, d2, m1));
         const unsigned long long old = atomicMin(bestS, k);
-        push = key_d2(old > k ? old : k);
+        push = old == k ? INFINITY : key_d2(old > k ? old : k);   // same point offered before: no loser
     }
     if (CERT) {
         if (__float_as_uint(push) < *(volatile unsigned*)cs.sec) atomicMin(cs.sec, __float_as_uint(push));
@@ -292,7 +295,7 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 //   __device__ void store(int i, unsigned long long best, float lb_out2)   (lb_out2 = 0: no certificate)
 //   CERT: store(int i, best, lb_out2, const int* list, int cnt, float rS2) with the candidate-
 //   leaf list (cnt leaves; every target outside them is at d2 >= rS2; cnt = 0: no list)
-//   float gap   (CERT only: the threshold margin g)
+//   float skin  (CERT only: the threshold margin g of the query just loaded)
 constexpr int kFrontierCap = 256;
 constexpr int kItemCap = 256;
 constexpr int kDirectLeaves = 256;
@@ -471,8 +474,6 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
     __shared__ unsigned sDrop[CERT ? kEngineWarps : 1][32];
     __shared__ float sThr[CERT ? kEngineWarps : 1][32];
     int* items = sItem[wid];
-    float g = 0.0f;
-    if constexpr (CERT) g = qs.gap;
     const float stale2 = qs.stale2;                         // warm-hint distance^2 that counts as stale
     const int npk = qs.packets(m);
     while (true) {
@@ -489,8 +490,10 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         int hint = -1;
         bool active = false;
         bool warm = false;
+        float g = 0.0f;                                       // CERT: this lane's threshold margin
         if (qi < m) {
             active = qs.load(qi, s, best, hint);
+            if constexpr (CERT) g = qs.skin;
             warm = hint >= 0;
             if (active && hint < 0) hint = coarse_hint_leaf(T, s);
         }
@@ -515,6 +518,34 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                 hint2 = coarse_hint_leaf(T, s);
                 if (hint2 != hint) eval_leaf_seq<B, CERT>(T, nq, hint2, best, sec);
                 else hint2 = -1;
+            }
+        }
+        // A2: the packet's queries are spatial neighbours: try the matches of the lanes +-1, +-2
+        // (an upper bound only -- their leaves are still evaluated in D/E if inside the ball)
+        {
+            const bool has = active && best != bound_key(cap2);
+            float4 tb = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (has) tb = __ldg(&T.opts[key_idx(best)]);
+            const uint32_t ib = has ? key_idx(best) : 0xffffffffu;
+#pragma unroll
+            for (int o = 1; o <= 2; ++o) {
+#pragma unroll
+                for (int dir = 0; dir < 2; ++dir) {
+                    const float x = dir ? __shfl_down_sync(FULL, tb.x, o) : __shfl_up_sync(FULL, tb.x, o);
+                    const float y = dir ? __shfl_down_sync(FULL, tb.y, o) : __shfl_up_sync(FULL, tb.y, o);
+                    const float z = dir ? __shfl_down_sync(FULL, tb.z, o) : __shfl_up_sync(FULL, tb.z, o);
+                    const uint32_t id = dir ? __shfl_down_sync(FULL, ib, o) : __shfl_up_sync(FULL, ib, o);
+                    const bool in = dir ? lane + o < 32 : lane >= o;
+                    if (active && in && id != 0xffffffffu) {
+                        const unsigned long long k = make_key(cand_d2(s, make_float4(x, y, z, 0.0f)), id);
+                        if (k < best) {
+                            // CERT: the replaced best loses (the hint leaf's minimum, or a point of
+                            // a leaf that D/E evaluates anyway -- an upper bound is conservative)
+                            if (CERT && best != bound_key(cap2)) sec = fminf(sec, key_d2(best));
+                            best = k;
+                        }
+                    }
+                }
             }
         }
         float thr = active ? thr_of(best) : 0.0f;

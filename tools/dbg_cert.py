@@ -17,7 +17,9 @@ def layout(m):
     L["pmask"] = L["gw"] + al(m * 4)
     L["plist"] = L["pmask"] + al((m + 31) // 32 * 4)
     L["gs"] = L["plist"] + al((m + 31) // 32 * 4)
-    L["vlist"] = L["gs"] + al(m * 4)
+    L["gd1"] = L["gs"] + al(m * 4)
+    L["gp"] = L["gd1"] + al(m * 4)
+    L["vlist"] = L["gp"] + al(m * 4)
     return L
 
 metric = "point_to_plane"

@@ -35,9 +35,9 @@ for f in (0.0, 1.0):
     print(f"iterate pose {f}: {e0.elapsed_time(e1)/5:.3f} ms", flush=True)
 
 P0 = d(np.eye(4))
-for cert, gap in ((True, 0.002), (True, 0.0005), (True, 0.006), (False, 0.0)):
+for cert, gap in ((True, (0.001, 0.005, 16.0)), (False, 0.0)):
     cil.set_certificates(cert)
-    if cert: cil.set_cert_gap(gap)
+    if cert: cil.set_cert_skin(*gap)
     for k in (1, 2, 5, 10, 20, 30, 50):
         pk = cil.make_params(metric, k, 1.0)
         cil.cil_icp_run(t, src, P0, pk, ws=ws, want_log=False)

@@ -113,6 +113,7 @@ _lib.cil_debug_set_cert_skin.argtypes = [C.c_double, C.c_double, C.c_double]
 
 # Byte offsets into the ICP workspace (csrc/icp.cu ws_layout, IcpState) -- diagnostics only.
 WS_STATE_SEARCHED = 176       # int64: sum over executed iterations of the search-list size
+WS_STATE_PCERT = 184          # int64: sum over executed iterations of point-certified points
 
 
 def set_certificates(on: bool = True) -> None:
@@ -123,6 +124,11 @@ def set_certificates(on: bool = True) -> None:
 def set_cert_skin(min_frac: float = 0.001, max_frac: float = 0.005, kappa: float = 16.0) -> None:
     """certificate skin of cil_icp_run: g = clamp(kappa * last-step displacement, min, max) x max_corr_dist"""
     _check(_lib.cil_debug_set_cert_skin(float(min_frac), float(max_frac), float(kappa)), "cil_debug_set_cert_skin")
+
+
+def run_point_certified(ws: torch.Tensor) -> int:
+    """points kept by the point certificate in cil_icp_run (sum over iterations; diagnostics)"""
+    return int(ws[WS_STATE_PCERT:WS_STATE_PCERT + 8].cpu().view(torch.int64).item())
 
 
 def run_searched(ws: torch.Tensor) -> int:

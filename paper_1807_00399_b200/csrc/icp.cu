@@ -264,6 +264,7 @@ struct SelWarp {
     unsigned long long best[32];
     unsigned sec[32];                        // point-level 2nd best (float bits)
     int items[32 * kListLeaves];
+    int npc;                                 // point-certified queries (diagnostics)
 };
 
 // leaf item for K_sel: best key and the point-level second best (the loser of every merge and
@@ -317,6 +318,7 @@ __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P,
                            Gp > 2.0f * displacement_bound(a.adelta + 16 * (wp & 255u), px, py, pz)) {
                     // point certificate (only where the leaf / list certificate holds too, so it
                     // never postpones a search): nn[i] stays, nothing to evaluate
+                    atomicAdd(&S.npc, 1);
                 } else {
                     const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
                     l0 = vl[0];
@@ -405,6 +407,7 @@ icp_select_kernel(const IterArgs a) {
     const uint32_t kslot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     if (threadIdx.x < 12) s_pose[threadIdx.x] = a.st->pose[threadIdx.x];
     if (threadIdx.x == 0) { s_cnt = 0; s_np = 0; }
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5].npc = 0;
     __syncthreads();
     Pose34 P;
 #pragma unroll
@@ -429,6 +432,9 @@ icp_select_kernel(const IterArgs a) {
     if (threadIdx.x == 0) {
         s_base = s_np ? atomicAdd(&a.st->plist_n, s_np) : 0;
         if (s_cnt) atomicAdd(&a.st->list_n, s_cnt);                    // diagnostics: searched points
+        int npc = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) npc += s_w[w].npc;
+        if (npc) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->pcert_n), (unsigned long long)npc);
     }
     __syncthreads();
     if (threadIdx.x < s_np) a.plist[s_base + threadIdx.x] = s_pk[threadIdx.x];
@@ -463,6 +469,7 @@ struct IcpQueries {
     int32_t* corr_idx;
     float* corr_d2;
     __device__ __forceinline__ int packets(int m) const { return plist ? *(volatile const int*)plist_n : (m + 31) / 32; }
+    __device__ __forceinline__ int tag() const { return (int)slot; }
     __device__ __forceinline__ int packet_base(int c) const { return 32 * (plist ? plist[c] : c); }
     __device__ __forceinline__ bool load(int i, DF3& s, unsigned long long& init, int& hint) const {
         if (pmask && !((pmask[i >> 5] >> (i & 31)) & 1u)) return false;    // certified in K_sel
@@ -607,7 +614,7 @@ __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
 template <int METRIC>
-__global__ void __launch_bounds__(kIcpThreads, 3)
+__global__ void __launch_bounds__(kIcpThreads, 2)
 icp_acc_kernel(const IterArgs a) {
     __shared__ double wsum[kIcpWarps][kSlots];
     __shared__ double Ssum[kSlots];
@@ -626,28 +633,34 @@ icp_acc_kernel(const IterArgs a) {
     for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
 
     const TargetView& T = a.T;
-    // two queries per trip with every load issued before the arithmetic (the gathers depend on
-    // nn[]; two independent chains in flight per thread); summation order = grid-stride order
+    // four queries per trip with every load issued before the arithmetic (the gathers depend on
+    // nn[]; four independent chains in flight per thread); summation order = grid-stride order
+    constexpr int U = 4;
     const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += 2 * stride) {
-        const int i1 = i + stride;
-        const int j0 = a.nn[i];
-        const int j1 = i1 < a.m ? a.nn[i1] : -1;
-        const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        float4 t0 = z4, t1 = z4, n0 = z4, n1 = z4;
-        float p0x = 0.0f, p0y = 0.0f, p0z = 0.0f, p1x = 0.0f, p1y = 0.0f, p1z = 0.0f;
-        if (j0 >= 0) {
-            t0 = __ldg(T.opts + j0);
-            if (METRIC == CIL_POINT_TO_PLANE) n0 = __ldg(T.onrm + j0);
-            p0x = a.src[3 * (size_t)i]; p0y = a.src[3 * (size_t)i + 1]; p0z = a.src[3 * (size_t)i + 2];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += U * stride) {
+        int jj[U];
+        float4 tt[U], nn4[U];
+        float px[U], py[U], pz[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + u * stride;
+            jj[u] = iu < a.m ? a.nn[iu] : -1;
         }
-        if (j1 >= 0) {
-            t1 = __ldg(T.opts + j1);
-            if (METRIC == CIL_POINT_TO_PLANE) n1 = __ldg(T.onrm + j1);
-            p1x = a.src[3 * (size_t)i1]; p1y = a.src[3 * (size_t)i1 + 1]; p1z = a.src[3 * (size_t)i1 + 2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + u * stride;
+            tt[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            nn4[u] = tt[u];
+            px[u] = py[u] = pz[u] = 0.0f;
+            if (jj[u] >= 0) {
+                tt[u] = __ldg(T.opts + jj[u]);
+                if (METRIC == CIL_POINT_TO_PLANE) nn4[u] = __ldg(T.onrm + jj[u]);
+                px[u] = a.src[3 * (size_t)iu]; py[u] = a.src[3 * (size_t)iu + 1]; pz[u] = a.src[3 * (size_t)iu + 2];
+            }
         }
-        if (j0 >= 0) accumulate_pair<METRIC>(acc, P, p0x, p0y, p0z, t0, n0, a.bound2);   // a3: j < 0 = rejected
-        if (j1 >= 0) accumulate_pair<METRIC>(acc, P, p1x, p1y, p1z, t1, n1, a.bound2);
+#pragma unroll
+        for (int u = 0; u < U; ++u)                                    // a3: nn < 0 = nothing within the bound
+            if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2);
     }
 
     // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
@@ -729,6 +742,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, 
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
         st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
+        st->pcert_n = 0;
     }
     for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; gp[i] = 0u; }
     if (iter_log)

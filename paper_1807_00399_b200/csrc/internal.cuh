@@ -61,6 +61,7 @@ struct alignas(256) IcpState {
     int list_n;           // 168: uncertified queries of the running iteration (diagnostics)
     int plist_n;          // 172: packets in the search list of the running iteration
     long long searched;   // 176: sum over executed iterations of list_n (diagnostics)
+    long long pcert_n;    // 184: sum over iterations of point-certified points (diagnostics)
 };
 
 // Certified warm start: anchor-pose ring of cil_icp_run.

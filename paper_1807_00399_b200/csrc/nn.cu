@@ -23,6 +23,7 @@ struct NNQueries {
     float* sqd;
     __device__ __forceinline__ int packets(int m) const { return (m + 31) / 32; }
     __device__ __forceinline__ int packet_base(int c) const { return 32 * c; }
+    __device__ __forceinline__ int tag() const { return 0; }
     __device__ __forceinline__ bool load(int k, DF3& s, unsigned long long& init, int& hint) const {
         const size_t i = perm[k];
         s.hx = q[3 * i]; s.hy = q[3 * i + 1]; s.hz = q[3 * i + 2];

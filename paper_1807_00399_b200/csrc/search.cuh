@@ -268,10 +268,10 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 //      packet box P = AABB of their balls B(s_i, sqrt(thr_i)) (conservatively inflated).
 //   C. every target inside P has a Morton key in [code(P.lo), code(P.hi)] (the key is
 //      monotone in each quantised coordinate and is computed by the same function), i.e. a
-//      contiguous sorted range [i0, i1) found by two binary searches: the candidate leaves
-//      are the leaves of that range whose box meets P -- tested directly (32 leaves per
-//      step) when the range is short, else by a breadth-first walk (one child box per lane,
-//      ballot compaction) from the lowest common ancestor of the range.
+//      contiguous sorted range, bracketed by the coarse-cell table: the candidate leaves are
+//      the leaves of that range whose box meets P -- tested directly (32 leaves per step)
+//      when the range is short, else by a breadth-first walk (one child box per lane, ballot
+//      compaction) from the lowest common ancestor of the range.
 //   D. every lane tests every candidate leaf against its own ball (lb^2 <= thr); the needed
 //      (leaf, query) pairs are appended, grouped by leaf, to a work list in shared memory.
 //   E. the work list is evaluated 32 items per round (any lane takes any item, so the number
@@ -298,7 +298,7 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 //   float skin  (CERT only: the threshold margin g of the query just loaded)
 constexpr int kFrontierCap = 256;
 constexpr int kItemCap = 256;
-constexpr int kDirectLeaves = 256;
+constexpr int kDirectLeaves = 1024;
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
 // Independent per-lane exact DFS (nearest-child first, a subtree is entered iff its lower
@@ -478,7 +478,8 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
     const int npk = qs.packets(m);
     while (true) {
         int c = 0;
-        if (lane == 0) c = (int)atomicAdd(counter, 1u);
+        // (read before claiming: warps of an almost empty work list leave without an atomic)
+        if (lane == 0) c = *(volatile unsigned*)counter >= (unsigned)npk ? npk : (int)atomicAdd(counter, 1u);
         c = __shfl_sync(FULL, c, 0);
         if (c >= npk) break;
         const int base = qs.packet_base(c);
@@ -603,12 +604,16 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             int* F = sF[wid][0];
             int* G = sF[wid][1];
             // ---- C: Morton range of P -> leaf range -> candidate leaves (node ids)
+            // (bracketed by the coarse-cell table: [first of code(P.lo)'s cell, first after
+            // code(P.hi)'s cell) is a superset of the key range -- two independent loads
+            // instead of a chain of binary-search steps)
             int ib = 0;
             if (lane < 2) {
                 const float4 Qz = __ldg(T.quant);
                 const unsigned long long code = lane == 0 ? morton_of(Qz, plo.x, plo.y, plo.z)
                                                           : morton_of(Qz, phi.x, phi.y, phi.z);
-                ib = key_bound(T, code, lane == 1);
+                const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
+                ib = (int)__ldg(T.cell_first + c + (lane == 1 ? 1u : 0u));
             }
             const int i0 = __shfl_sync(FULL, ib, 0), i1 = __shfl_sync(FULL, ib, 1);
             int nF = 0;
@@ -616,17 +621,27 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             if (i1 > i0) {
                 const int la = i0 / B, lb = (i1 - 1) / B;
                 if (lb - la < kDirectLeaves) {
-                    for (int b0 = la; b0 <= lb; b0 += 32) {
-                        const int f = b0 + lane;
-                        bool hit = false;
-                        if (f <= lb) {
-                            const float4* bx = T.box + 2 * (size_t)(l_pad + f);
-                            hit = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
+                    // 4 x 32 leaves per step, all box loads in flight together
+                    for (int b0 = la; b0 <= lb; b0 += 128) {
+                        bool hit[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int f = b0 + 32 * u + lane;
+                            hit[u] = false;
+                            if (f <= lb) {
+                                const float4* bx = T.box + 2 * (size_t)(l_pad + f);
+                                hit[u] = box_meets(__ldg(bx), __ldg(bx + 1), plo, phi);
+                            }
                         }
-                        const unsigned mk = __ballot_sync(FULL, hit);
-                        if (hit) F[nF + __popc(mk & lt)] = f;
-                        nF += __popc(mk);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned mk = __ballot_sync(FULL, hit[u]);
+                            const int pos = nF + __popc(mk & lt);
+                            if (hit[u] && pos < kFrontierCap) F[pos] = b0 + 32 * u + lane;
+                            nF += __popc(mk);
+                        }
                     }
+                    if (nF > kFrontierCap) overflow = true;
                 } else {
                     int a = l_pad + la;
                     const int k = 32 - __clz(a ^ (l_pad + lb));
@@ -670,43 +685,53 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                 if (CERT) sSec[wid][lane] = __float_as_uint(sec);
                 __syncwarp();
                 int nI = 0;
-                for (int k = 0; k < nF; ++k) {
-                    const int f = F[k];
-                    const float lb = leaf_lb2(T, nq, f);
-                    const bool need = normal && f != hint && f != hint2 && lb <= thr;
-                    const unsigned mk = __ballot_sync(FULL, need);
-                    if (need) items[nI + __popc(mk & lt)] = (f << 5) | lane;
-                    nI += __popc(mk);
-                    if (tracing) dbg_items += need ? 1 : 0;
-                    if (nI > kItemCap - 32 || (k == nF - 1 && nI > 0)) {
-                        __syncwarp();
-                        for (int r0 = 0; r0 < nI; r0 += 32) {
-                            const int j = r0 + lane;
-                            if (j < nI) {
-                                const int it = items[j];
-                                const int q = it & 31;
-                                NegQuery qq;
-                                qq.hx = make_float2(sQ[wid][0][q], sQ[wid][0][q]);
-                                qq.hy = make_float2(sQ[wid][1][q], sQ[wid][1][q]);
-                                qq.hz = make_float2(sQ[wid][2][q], sQ[wid][2][q]);
-                                qq.lx = make_float2(sQ[wid][3][q], sQ[wid][3][q]);
-                                qq.ly = make_float2(sQ[wid][4][q], sQ[wid][4][q]);
-                                qq.lz = make_float2(sQ[wid][5][q], sQ[wid][5][q]);
-                                CertSlots cs;
-                                if (CERT) {
-                                    cs.sec = &sSec[wid][q]; cs.list = sList[wid][q]; cs.cnt = &sCnt[wid][q];
-                                    cs.drop = &sDrop[wid][q]; cs.thr = &sThr[wid][q];
-                                }
-                                eval_leaf_item<B, CERT>(T, qq, it >> 5, &sBest[wid][q], cs);
+                // evaluate the collected items (32 per round) and refresh the lane thresholds
+                auto flush = [&]() {
+                    __syncwarp();
+                    for (int r0 = 0; r0 < nI; r0 += 32) {
+                        const int jj = r0 + lane;
+                        if (jj < nI) {
+                            const int it = items[jj];
+                            const int q = it & 31;
+                            NegQuery qq;
+                            qq.hx = make_float2(sQ[wid][0][q], sQ[wid][0][q]);
+                            qq.hy = make_float2(sQ[wid][1][q], sQ[wid][1][q]);
+                            qq.hz = make_float2(sQ[wid][2][q], sQ[wid][2][q]);
+                            qq.lx = make_float2(sQ[wid][3][q], sQ[wid][3][q]);
+                            qq.ly = make_float2(sQ[wid][4][q], sQ[wid][4][q]);
+                            qq.lz = make_float2(sQ[wid][5][q], sQ[wid][5][q]);
+                            CertSlots cs;
+                            if (CERT) {
+                                cs.sec = &sSec[wid][q]; cs.list = sList[wid][q]; cs.cnt = &sCnt[wid][q];
+                                cs.drop = &sDrop[wid][q]; cs.thr = &sThr[wid][q];
                             }
+                            eval_leaf_item<B, CERT>(T, qq, it >> 5, &sBest[wid][q], cs);
                         }
-                        __syncwarp();
-                        nI = 0;
-                        best = sBest[wid][lane];
-                        if (CERT) sec = __uint_as_float(sSec[wid][lane]);
-                        if (active) thr = thr_of(best);
-                        if (CERT) sThr[wid][lane] = thr;
                     }
+                    __syncwarp();
+                    nI = 0;
+                    best = sBest[wid][lane];
+                    if (CERT) sec = __uint_as_float(sSec[wid][lane]);
+                    if (active) thr = thr_of(best);
+                    if (CERT) sThr[wid][lane] = thr;
+                };
+                // four candidate leaves per step: their box loads are in flight together
+                for (int k = 0; k < nF; k += 4) {
+                    int f[4];
+                    float lb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) f[u] = k + u < nF ? F[k + u] : -1;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, nq, f[u]) : INFINITY;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool need = normal && f[u] >= 0 && f[u] != hint && f[u] != hint2 && lb[u] <= thr;
+                        const unsigned mk = __ballot_sync(FULL, need);
+                        if (need) items[nI + __popc(mk & lt)] = (f[u] << 5) | lane;
+                        nI += __popc(mk);
+                        if (tracing) dbg_items += need ? 1 : 0;
+                    }
+                    if (nI > kItemCap - 128 || (k + 4 >= nF && nI > 0)) flush();
                 }
             }
         }
@@ -720,6 +745,8 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             rec[5] = __float_as_int(key_d2(best));
             rec[6] = dbg_items;
             rec[8] = (int)(ckA - ck0); rec[9] = (int)(ckB - ckA); rec[10] = (int)(ckC - ckB); rec[11] = (int)(ckD - ckC);
+            rec[13] = qs.tag();
+            rec[14] = __popc(__ballot_sync(__activemask(), active));
         }
         // ---- F: exact ballot DFS for outliers (or everyone after an overflow)
         // sparse packet: independent per-lane DFS; outliers / overflow: ballot DFS

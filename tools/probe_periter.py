@@ -29,20 +29,23 @@ for gap, fl in itertools.product(gaps, flags):
         res, _ = cil.cil_icp_run(t, src, P0, prm, ws=ws, want_log=False)
         torch.cuda.synchronize()
         pr = cil.profile_read(); cil.profile_enable(False)
-        cur = (pr["sel_ms"], pr["nn_ms"], pr["acc_ms"], cil.run_searched(ws), cil.decode_result(res).pose)
+        cur = (pr["sel_ms"], pr["nn_ms"], pr["acc_ms"], cil.run_searched(ws), cil.decode_result(res).pose,
+               cil.run_point_certified(ws))
         if prev is None:
             dsel, dnn, dacc, dsr = cur[0], cur[1], cur[2], cur[3]
+            dpc = cur[5]
             step = np.nan
         else:
             dsel, dnn, dacc, dsr = (cur[i] - prev[i] for i in range(4))
+            dpc = cur[5] - prev[5]
             dP = np.linalg.inv(prev[4]) @ cur[4]
             ang = np.arccos(np.clip((np.trace(dP[:3, :3]) - 1) / 2, -1, 1))
             step = ang * R + np.linalg.norm(dP[:3, 3])     # displacement bound at the max range
-        rows.append((k - 1, dsel * 1e3, dnn * 1e3, dacc * 1e3, dsr / w.m, step))
+        rows.append((k - 1, dsel * 1e3, dnn * 1e3, dacc * 1e3, dsr / w.m, step, dpc / w.m))
         prev = cur
     print(f"gap {gap} flags {fl}: iteration | sel us | nn us | acc us | searched frac | step bound m (prev->this)")
     for r in rows:
-        print(f"  {r[0]:3d} {r[1]:8.1f} {r[2]:8.1f} {r[3]:7.1f}  {r[4]:6.3f}  {r[5]:.3g}", flush=True)
+        print(f"  {r[0]:3d} {r[1]:8.1f} {r[2]:8.1f} {r[3]:7.1f}  {r[4]:6.3f}  {r[5]:.3g}  pcert {r[6]:.3f}", flush=True)
     tot = sum(r[1] + r[2] + r[3] for r in rows)
     print(f"  TOTAL gap {gap} flags {fl}: {tot/1e3:.2f} ms (first 10: {sum(r[1]+r[2]+r[3] for r in rows[:10])/1e3:.2f}), "
           f"full-equiv {sum(r[4] for r in rows):.2f}", flush=True)

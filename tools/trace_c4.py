@@ -65,8 +65,16 @@ for k in (40,):
     torch.cuda.synchronize()
     cil.lib().cil_debug_engine_trace(None)
     a = tr.cpu().numpy().reshape(-1, 16)
-    n_last = int((a[:, 8] != 0).sum())   # slots of the last (smallest) list are overwritten last
-    print("cert run: slots with a trace record", n_last, "(records of the last iterations overlap)")
-    fl = a[:, 0]
-    print("  flags: normal", int((fl & 1).sum()), "outlier", int(((fl >> 1) & 1).sum()), "overflow", int(((fl >> 2) & 1).sum()),
-          "sparse", int(((fl >> 3) & 1).sum()))
+    for it in (k - 3, k - 2, k - 1):
+        sel = (a[:, 8] != 0) & (a[:, 13] == it)
+        r = a[sel]
+        if len(r) == 0:
+            print("cert run iteration", it, "no searched slots"); continue
+        fl = r[:, 0]
+        ck = r[:, 8:13].astype(np.float64)
+        tot = ck.sum(1)
+        print(f"cert run iteration {it}: searched slots {len(r)}, active lanes/packet mean {r[:, 14].mean():.1f}, "
+              f"normal {(fl & 1).mean():.3f} outlier {((fl >> 1) & 1).mean():.3f} overflow {((fl >> 2) & 1).mean():.3f} "
+              f"sparse {((fl >> 3) & 1).mean():.3f}")
+        print(f"   clocks per packet (lane view) p50 {np.percentile(tot, 50):.0f} p90 {np.percentile(tot, 90):.0f} max {tot.max():.0f}; "
+              f"mean share A,B,C,DE,F {(ck.sum(0) / ck.sum()).round(3).tolist()}; nF mean {r[:, 4].mean():.1f} items mean {r[:, 6].mean():.1f}")

@@ -121,13 +121,34 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- our arm
+def reduce_over_ranks(tot_ms: float, pairs: float, world: int, device) -> tuple[float, float]:
+    """Whole-job aggregation: the timed region's duration is the MAX over ranks (device-timed
+    per rank), the work is the SUM of every rank's point-pairs (each rank aligns its own
+    frame pair: weak scaling, no data-path collective)."""
+    if world == 1:
+        return tot_ms, pairs
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    p = torch.tensor([pairs], dtype=torch.float64, device=device)
+    dist.all_reduce(p, op=dist.ReduceOp.SUM)
+    dist.barrier()
+    return float(t.item()), float(p.item())
+
+
+def rank_seed(rank: int) -> int:
+    """seed base of the frame pair rank `rank` aligns (rank 0 = BASELINE.json's configs)"""
+    return 1807 + rank
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1807_00399_b200 as cil
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    w = _workload(args.workload, 1807 + rank)
+    w = _workload(args.workload, rank_seed(rank))
     iters = args.iters or w.max_iters
     metric = w.metric
     to_dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
@@ -177,17 +198,7 @@ def run_ours(args, rank, world, local_rank):
     cil.profile_enable(False)
     prof = cil.profile_read()
     launches = cil.launch_count() - launches0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_max = float(t.item())
-        pairs = torch.tensor([float(w.m) * iters * args.steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(pairs, op=dist.ReduceOp.SUM)
-        total_pairs = float(pairs.item())
-        dist.barrier()
-    else:
-        tot_max, total_pairs = tot_ms, float(w.m) * iters * args.steps
+    tot_max, total_pairs = reduce_over_ranks(tot_ms, float(w.m) * iters * args.steps, world, dev)
     r = cil.decode_result(res)
     if rank != 0:
         return None

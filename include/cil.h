@@ -62,7 +62,9 @@ typedef enum {
 
 typedef enum {
     CIL_POINT_TO_POINT = 0,    /* r = s - t,        J = [-[s]x , I3]  [Besl & McKay]  */
-    CIL_POINT_TO_PLANE = 1     /* r = (s - t).n,    J = [s x n ; n]   [Low 2004]      */
+    CIL_POINT_TO_PLANE = 1,    /* r = (s - t).n,    J = [s x n ; n]   [Low 2004]      */
+    CIL_COMBINED = 2           /* w_point |s - t|^2 + w_plane ((s - t).n)^2: the weighted
+                                  combination the paper names (R22) */
 } cil_metric;
 
 typedef struct cil_target cil_target;   /* opaque, immutable after build */
@@ -78,8 +80,9 @@ typedef struct {
    max_corr_dist > 0: pairs with |s - t| > max_corr_dist are rejected (inclusive bound,
    PAPER.md:195, R2).  rot_tol (rad) / trans_tol: cil_icp_run stops after an
    iteration whose increment has angle < rot_tol AND |tau| < trans_tol (both 0 = fixed
-   iteration count).  w_point/w_plane: reserved for the combined metric
-   (must be 0). */
+   iteration count).  w_point/w_plane: the weights of CIL_COMBINED (finite,
+   >= 0, not both 0; H = w_point H_point + w_plane H_plane, likewise g and the squared-residual
+   sum); must be 0 for the single metrics.  Point-to-plane and combined need target normals. */
 typedef struct {
     int32_t metric;
     int32_t max_iters;

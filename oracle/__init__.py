@@ -27,7 +27,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 OK, DEGENERATE, NO_CORRESPONDENCES = 0, 16, 17
-METRICS = {"point_to_point": 0, "point_to_plane": 1}
+METRICS = {"point_to_point": 0, "point_to_plane": 1, "combined": 2}
 
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
@@ -61,6 +61,8 @@ def lib():
         L.orc_kd_free.argtypes = [C.c_void_p]
         L.orc_knn.argtypes = [C.c_void_p, _f32p, C.c_int64, _f64p, C.c_int64, C.c_int, C.c_double, _i64p, _f64p]
         L.orc_transform.argtypes = [_f64p, _f32p, C.c_int64, _f64p]
+        L.orc_set_combined_weights.argtypes = [C.c_double, C.c_double]
+        L.orc_set_combined_weights.restype = None
         L.orc_icp_system.argtypes = [C.c_void_p, _f32p, _opt(_f32p), C.c_int64, _f32p, C.c_int64, _f64p, C.c_int,
                                      C.c_double, _f64p, _f64p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                      _opt(_f64p), _opt(_f64p), _opt(_i64p), _opt(_f64p), _opt(_f64p)]
@@ -77,6 +79,11 @@ def lib():
         L.orc_pca_normals.argtypes = [C.c_void_p, _f32p, C.c_int64, C.c_int, _f64p, _f32p, _opt(_f32p)]
         _lib = L
     return _lib
+
+
+def set_combined_weights(w_point: float, w_plane: float) -> None:
+    """weights of metric "combined" (w_point * point-to-point + w_plane * point-to-plane)"""
+    lib().orc_set_combined_weights(float(w_point), float(w_plane))
 
 
 def set_threads(n: int) -> None:

@@ -266,11 +266,38 @@ int orc_knn(const void* kd, const float* pts, int64_t n, const double* q, int64_
 /* ------------------------------------------------------------------ normal equations */
 #define MET_P2POINT 0
 #define MET_P2PLANE 1
+#define MET_COMBINED 2   /* w_point * point-to-point + w_plane * point-to-plane ("weighted combinations") */
+
+static double g_w_point = 0.0, g_w_plane = 0.0;
+
+/* weights of MET_COMBINED (reading R22) */
+void orc_set_combined_weights(double w_point, double w_plane) {
+    g_w_point = w_point;
+    g_w_plane = w_plane;
+}
 
 /* add one accepted pair (s, t, n) to H, g, sse and the absolute-value scales */
 static void add_pair(int metric, const double s[3], const float* tp, const float* np_,
                      double H[36], double g[6], double* sse, double Habs[36], double gabs[6]) {
     double t[3] = {tp[0], tp[1], tp[2]};
+    if (metric == MET_COMBINED) {
+        /* the weighted sum of the two single-metric contributions of this pair */
+        double Hp[36] = {0}, gp[6] = {0}, sp = 0.0, Hl[36] = {0}, gl[6] = {0}, sl = 0.0;
+        add_pair(MET_P2POINT, s, tp, np_, Hp, gp, &sp, NULL, NULL);
+        add_pair(MET_P2PLANE, s, tp, np_, Hl, gl, &sl, NULL, NULL);
+        for (int a = 0; a < 36; ++a) {
+            const double v = g_w_point * Hp[a] + g_w_plane * Hl[a];
+            H[a] += v;
+            if (Habs) Habs[a] += fabs(v);
+        }
+        for (int a = 0; a < 6; ++a) {
+            const double v = g_w_point * gp[a] + g_w_plane * gl[a];
+            g[a] += v;
+            if (gabs) gabs[a] += fabs(v);
+        }
+        *sse += g_w_point * sp + g_w_plane * sl;
+        return;
+    }
     if (metric == MET_P2PLANE) {
         double n[3] = {np_[0], np_[1], np_[2]};
         double d[3] = {s[0] - t[0], s[1] - t[1], s[2] - t[2]};
@@ -316,7 +343,7 @@ int orc_icp_system(const void* kd, const float* tgt, const float* nrm, int64_t n
                    double H[36], double g[6], double* sse, int64_t* count,
                    double* Habs, double* gabs,
                    int64_t* corr_idx, double* corr_d2, double* corr_d2nd) {
-    if (metric == MET_P2PLANE && !nrm) return 3;
+    if ((metric == MET_P2PLANE || metric == MET_COMBINED) && !nrm) return 3;
     double bound2 = max_dist * max_dist;
     int64_t* ci = (int64_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(int64_t));
     double* s = (double*)malloc((size_t)(m > 0 ? m : 1) * 3 * sizeof(double));
@@ -352,7 +379,7 @@ int orc_icp_system_from_corr(const float* tgt, const float* nrm, int64_t n, cons
                              const double pose[16], int metric, const int32_t* corr,
                              double H[36], double g[6], double* sse, int64_t* count,
                              double* Habs, double* gabs) {
-    if (metric == MET_P2PLANE && !nrm) return 3;
+    if ((metric == MET_P2PLANE || metric == MET_COMBINED) && !nrm) return 3;
     memset(H, 0, 36 * sizeof(double));
     memset(g, 0, 6 * sizeof(double));
     if (Habs) memset(Habs, 0, 36 * sizeof(double));

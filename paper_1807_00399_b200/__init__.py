@@ -39,7 +39,8 @@ CIL_ERR_DEGENERATE = 16
 CIL_NO_CORRESPONDENCES = 17
 CIL_POINT_TO_POINT = 0
 CIL_POINT_TO_PLANE = 1
-METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_PLANE}
+CIL_COMBINED = 2
+METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_PLANE, "combined": CIL_COMBINED}
 
 EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
@@ -190,15 +191,16 @@ def _pts(t: torch.Tensor, name: str) -> torch.Tensor:
 
 
 def make_params(metric: str | int = "point_to_plane", max_iters: int = 1, max_corr_dist: float = math.inf,
-                rot_tol: float = 0.0, trans_tol: float = 0.0) -> cil_icp_params:
+                rot_tol: float = 0.0, trans_tol: float = 0.0, w_point: float = 0.0,
+                w_plane: float = 0.0) -> cil_icp_params:
     p = cil_icp_params()
     p.metric = METRICS[metric] if isinstance(metric, str) else int(metric)
     p.max_iters = int(max_iters)
     p.max_corr_dist = float(max_corr_dist)
     p.rot_tol = float(rot_tol)
     p.trans_tol = float(trans_tol)
-    p.w_point = 0.0
-    p.w_plane = 0.0
+    p.w_point = float(w_point)
+    p.w_plane = float(w_plane)
     return p
 
 

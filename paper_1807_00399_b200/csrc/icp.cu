@@ -43,6 +43,7 @@ struct IterArgs {
     const float* src;
     int m;
     float bound2;            // fl32(max_corr_dist^2): acceptance (a3)
+    float w_pp, w_pl;        // CIL_COMBINED weights (fl32 of w_point, w_plane)
     float search2;           // search bound: bound2, or fl32(rho^2) with certificates
     float gap_none;          // certificate of "no target within rho": rho - max_corr_dist (rounded down)
     float gap_min, gap_max, kappa;   // per-point certificate skin clamp(kappa * last step, gap_min, gap_max)
@@ -108,7 +109,7 @@ __device__ __noinline__ void rodrigues(const double a[3], double R[9]) {
 // Build (H, g, sse, count) from the reduced sums of the metric.
 template <int METRIC>
 __device__ __noinline__ void assemble(const double* S, double H[36], double g[6], double& sse, double& cnt) {
-    if (METRIC == CIL_POINT_TO_PLANE) {
+    if (METRIC != CIL_POINT_TO_POINT) {          // point-to-plane and combined: 21 + 6 + sse + count
         int k = 0;
         for (int a = 0; a < 6; ++a)
             for (int b = a; b < 6; ++b, ++k) { H[6 * a + b] = S[k]; H[6 * b + a] = S[k]; }
@@ -579,13 +580,39 @@ icp_nn_kernel(const IterArgs a) {
 // Jacobian, fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
 template <int METRIC>
 __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose34& P, float px, float py, float pz,
-                                                float4 t, float4 n, float bound2) {
+                                                float4 t, float4 n, float bound2, float wpp, float wpl) {
     const DF3 s = transform_df(P, px, py, pz);
     const float dx = dfdiff(s.hx, s.lx, t.x);
     const float dy = dfdiff(s.hy, s.ly, t.y);
     const float dz = dfdiff(s.hz, s.lz, t.z);
     if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= bound2)) return;
-    if (METRIC == CIL_POINT_TO_PLANE) {
+    if (METRIC == CIL_COMBINED) {
+        // w_pl J_pl J_pl^T + w_pp J_pp^T J_pp per pair, J_pp = [-[s]x, I3] (R22): the
+        // point-to-point blocks are |s|^2 I - s s^T, [s]x, I written out per pair (no
+        // cross-pair cancellation), in the 21 + 6 + sse + count layout of point-to-plane
+        const float sx = s.hx, sy = s.hy, sz = s.hz;
+        const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
+        const float J[6] = {fmaf(sy, n.z, -sz * n.y), fmaf(sz, n.x, -sx * n.z), fmaf(sx, n.y, -sy * n.x),
+                            n.x, n.y, n.z};
+        // H_pp upper triangle, row-major over (0..5) x (p..5)
+        const float Hp[21] = {fmaf(sy, sy, sz * sz), -sx * sy, -sx * sz, 0.0f, -sz, sy,
+                              fmaf(sx, sx, sz * sz), -sy * sz, sz, 0.0f, -sx,
+                              fmaf(sx, sx, sy * sy), -sy, sx, 0.0f,
+                              1.0f, 0.0f, 0.0f,
+                              1.0f, 0.0f,
+                              1.0f};
+        // g_pp = [s x r_pp; r_pp], r_pp = s - t
+        const float gp[6] = {fmaf(sy, dz, -sz * dy), fmaf(sz, dx, -sx * dz), fmaf(sx, dy, -sy * dx), dx, dy, dz};
+        int k = 0;
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+            for (int q = p; q < 6; ++q, ++k) acc[k] = fmaf(wpl * J[p], J[q], fmaf(wpp, Hp[k], acc[k]));
+#pragma unroll
+        for (int p = 0; p < 6; ++p) acc[21 + p] = fmaf(wpl * J[p], r, fmaf(wpp, gp[p], acc[21 + p]));
+        acc[27] = fmaf(wpl * r, r, fmaf(wpp, fmaf(dx, dx, fmaf(dy, dy, dz * dz)), acc[27]));
+        acc[28] += 1.0f;
+    } else if (METRIC == CIL_POINT_TO_PLANE) {
         const float r = fmaf(dx, n.x, fmaf(dy, n.y, dz * n.z));
         const float J[6] = {fmaf(s.hy, n.z, -s.hz * n.y), fmaf(s.hz, n.x, -s.hx * n.z),
                             fmaf(s.hx, n.y, -s.hy * n.x), n.x, n.y, n.z};
@@ -654,13 +681,13 @@ icp_acc_kernel(const IterArgs a) {
             px[u] = py[u] = pz[u] = 0.0f;
             if (jj[u] >= 0) {
                 tt[u] = __ldg(T.opts + jj[u]);
-                if (METRIC == CIL_POINT_TO_PLANE) nn4[u] = __ldg(T.onrm + jj[u]);
+                if (METRIC != CIL_POINT_TO_POINT) nn4[u] = __ldg(T.onrm + jj[u]);
                 px[u] = a.src[3 * (size_t)iu]; py[u] = a.src[3 * (size_t)iu + 1]; pz[u] = a.src[3 * (size_t)iu + 2];
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)                                    // a3: nn < 0 = nothing within the bound
-            if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2);
+            if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2, a.w_pp, a.w_pl);
     }
 
     // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
@@ -826,8 +853,11 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
     count_launches(n);
     cudaError_t e = a.cert ? launch_nn_t<true>(a, s) : launch_nn_t<false>(a, s);
     if (e != cudaSuccess) return e;
-    return metric == CIL_POINT_TO_PLANE ? launch_acc_m<CIL_POINT_TO_PLANE>(a, s)
-                                        : launch_acc_m<CIL_POINT_TO_POINT>(a, s);
+    switch (metric) {
+        case CIL_POINT_TO_PLANE: return launch_acc_m<CIL_POINT_TO_PLANE>(a, s);
+        case CIL_COMBINED: return launch_acc_m<CIL_COMBINED>(a, s);
+        default: return launch_acc_m<CIL_POINT_TO_POINT>(a, s);
+    }
 }
 
 struct WsLayout {
@@ -872,18 +902,29 @@ void bind_ws(IterArgs& a, void* ws, int64_t m) {
 
 cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
                         void* ws, size_t ws_bytes) {
-    if (!t || !p) { set_error("%s: NULL target or params", fn); return CIL_ERR_INVALID_ARG; }
-    if (m < 0 || m > INT32_MAX) { set_error("%s: m=%lld out of range", fn, (long long)m); return CIL_ERR_INVALID_ARG; }
-    if (m > 0 && !src) { set_error("%s: src is NULL", fn); return CIL_ERR_INVALID_ARG; }
-    if (p->metric != CIL_POINT_TO_POINT && p->metric != CIL_POINT_TO_PLANE) {
+    // parameters first (host-only, no target needed), then the target and buffers
+    if (!p) { set_error("%s: NULL params", fn); return CIL_ERR_INVALID_ARG; }
+    if (p->metric != CIL_POINT_TO_POINT && p->metric != CIL_POINT_TO_PLANE && p->metric != CIL_COMBINED) {
         set_error("%s: metric %d not supported", fn, p->metric);
+        return CIL_ERR_INVALID_ARG;
+    }
+    if (p->metric == CIL_COMBINED) {
+        if (!(p->w_point >= 0.0) || !(p->w_plane >= 0.0) || !(p->w_point + p->w_plane > 0.0) ||
+            !std::isfinite(p->w_point) || !std::isfinite(p->w_plane)) {
+            set_error("%s: combined metric needs finite weights >= 0, not both 0", fn);
+            return CIL_ERR_INVALID_ARG;
+        }
+    } else if (p->w_point != 0.0 || p->w_plane != 0.0) {
+        set_error("%s: w_point/w_plane are only used by CIL_COMBINED (must be 0)", fn);
         return CIL_ERR_INVALID_ARG;
     }
     if (!(p->max_corr_dist > 0.0)) { set_error("%s: max_corr_dist must be > 0", fn); return CIL_ERR_INVALID_ARG; }
     if (!(p->rot_tol >= 0.0) || !(p->trans_tol >= 0.0)) { set_error("%s: tolerances must be >= 0", fn); return CIL_ERR_INVALID_ARG; }
-    if (p->w_point != 0.0 || p->w_plane != 0.0) { set_error("%s: w_point/w_plane are reserved (0)", fn); return CIL_ERR_INVALID_ARG; }
-    if (p->metric == CIL_POINT_TO_PLANE && !t->has_normals) {
-        set_error("%s: point-to-plane needs a target built with normals", fn);
+    if (!t) { set_error("%s: NULL target", fn); return CIL_ERR_INVALID_ARG; }
+    if (m < 0 || m > INT32_MAX) { set_error("%s: m=%lld out of range", fn, (long long)m); return CIL_ERR_INVALID_ARG; }
+    if (m > 0 && !src) { set_error("%s: src is NULL", fn); return CIL_ERR_INVALID_ARG; }
+    if ((p->metric == CIL_POINT_TO_PLANE || p->metric == CIL_COMBINED) && !t->has_normals) {
+        set_error("%s: point-to-plane / combined need a target built with normals", fn);
         return CIL_ERR_NO_NORMALS;
     }
     if (!ws || ((uintptr_t)ws & 255u)) { set_error("%s: workspace NULL or not 256-B aligned", fn); return CIL_ERR_WORKSPACE; }
@@ -922,6 +963,8 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     a.m = (int)m;
     a.bound2 = bound2_of(params->max_corr_dist);
     a.search2 = a.bound2;
+    a.w_pp = (float)params->w_point;
+    a.w_pl = (float)params->w_plane;
     a.pose_in = pose_in;
     a.pose_out = pose_out;
     a.sys = sys;
@@ -950,6 +993,8 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.src = src;
     a.m = (int)m;
     a.bound2 = bound2_of(params->max_corr_dist);
+    a.w_pp = (float)params->w_point;
+    a.w_pl = (float)params->w_plane;
     a.cert = (debug_flags() & 1u) ? 0 : 1;
     a.point_cert = (debug_flags() & 8u) ? 0 : 1;
     // certificates search to rho = 1.1 max_corr_dist so that a point with

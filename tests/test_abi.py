@@ -103,3 +103,20 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "orc_" not in txt, f
+
+
+def test_combined_metric_parameter_errors(cil):
+    """CIL_COMBINED: weights finite, >= 0, not both 0; the single
+    metrics keep w_point = w_plane = 0.  Rejected on the host, before the target is touched."""
+    L = cil.lib()
+    for wp, wl in ((0.0, 0.0), (-1.0, 1.0), (1.0, float("nan")), (float("inf"), 1.0)):
+        p = cil.make_params("combined", 5, 0.1, w_point=wp, w_plane=wl)
+        assert L.cil_icp_run(None, None, 10, None, C.byref(p), None, 0, None, None, None) == cil.CIL_ERR_INVALID_ARG
+        assert "weights" in L.cil_last_error().decode()
+    p = cil.make_params("point_to_plane", 5, 0.1, w_point=1.0)
+    assert L.cil_icp_iterate(None, None, 10, None, C.byref(p), None, 0, None, None, None, None, None) == \
+        cil.CIL_ERR_INVALID_ARG
+    assert "CIL_COMBINED" in L.cil_last_error().decode()
+    ok = cil.make_params("combined", 5, 0.1, w_point=0.5, w_plane=1.0)
+    assert L.cil_icp_run(None, None, 10, None, C.byref(ok), None, 0, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    assert "target" in L.cil_last_error().decode()        # parameters passed; the NULL target is next

@@ -137,11 +137,21 @@ def _perturb(gt, frac):
     return _pose(Rotation.from_rotvec(rv).as_matrix(), gt[:3, 3] * frac)
 
 
+COMBINED_W = (0.4, 1.3)   # weights of the combined metric in these tests
+
+
+def _params(cil, metric, iters, max_dist):
+    if metric == "combined":
+        oracle.set_combined_weights(*COMBINED_W)
+        return cil.make_params(metric, iters, max_dist, w_point=COMBINED_W[0], w_plane=COMBINED_W[1])
+    return cil.make_params(metric, iters, max_dist)
+
+
 def check_iteration(cil, w, pose, metric, tree=None, sample=None, leaf=0):
     """cil_icp_iterate vs oracle at the same pose_in: correspondences, H, g, pose_out."""
     t = cil.cil_target_build(dev(w.target), dev(w.target_normals) if w.target_normals is not None else None,
                              leaf_size=leaf)
-    prm = cil.make_params(metric, 1, w.max_dist)
+    prm = _params(cil, metric, 1, w.max_dist)
     P = dev(pose.astype(np.float64))
     pose_out, sys_t, ci, cd = cil.cil_icp_iterate(t, dev(w.source), P, prm, want_corr=True)
     gs = cil.decode_system(sys_t)
@@ -182,9 +192,9 @@ def test_iterate_c1(cil, frac):
     check_iteration(cil, w, _perturb(w.gt_pose, frac), "point_to_plane")
 
 
-@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point", "combined"])
 def test_iterate_c4_reduced(cil, metric):
-    w = W.c4(metric, rings=16, az=8000)
+    w = W.c4("point_to_plane" if metric == "combined" else metric, rings=16, az=8000)
     for frac in (0.0, 0.5, 1.0):
         check_iteration(cil, w, _perturb(w.gt_pose, frac), metric)
 
@@ -210,7 +220,7 @@ def test_iterate_leaf_sizes(cil, leaf):
 def check_run(cil, w, metric, leaf=0):
     t = cil.cil_target_build(dev(w.target), dev(w.target_normals) if w.target_normals is not None else None,
                              leaf_size=leaf)
-    prm = cil.make_params(metric, w.max_iters, w.max_dist)
+    prm = _params(cil, metric, w.max_iters, w.max_dist)
     res_t, log = cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)
     res = cil.decode_result(res_t)
     o = oracle.icp_run(None, w.target_normals, w.source, metric, w.max_iters, w.max_dist, tree=W.oracle_tree(w))
@@ -236,9 +246,22 @@ def test_run_c1(cil):
     check_run(cil, W.c1(), "point_to_plane")
 
 
-@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point", "combined"])
 def test_run_c4_reduced(cil, metric):
-    check_run(cil, W.c4(metric, rings=16, az=8000), metric)
+    check_run(cil, W.c4("point_to_plane" if metric == "combined" else metric, rings=16, az=8000), metric)
+
+
+@pytest.mark.parametrize("w", [(1.0, 0.0), (0.0, 1.0)])
+def test_combined_reduces_to_single_metrics_gpu(cil, w):
+    """NEXT-1 pin on the GPU path: combined (1,0) / (0,1) runs end at the single-metric poses."""
+    wl = W.c4("point_to_plane", rings=8, az=4000)
+    t = cil.cil_target_build(dev(wl.target), dev(wl.target_normals))
+    single = "point_to_point" if w[0] == 1.0 else "point_to_plane"
+    a = cil.decode_result(cil.cil_icp_run(t, dev(wl.source), dev(np.eye(4)),
+                                          cil.make_params("combined", 10, 1.0, w_point=w[0], w_plane=w[1]))[0])
+    b = cil.decode_result(cil.cil_icp_run(t, dev(wl.source), dev(np.eye(4)), cil.make_params(single, 10, 1.0))[0])
+    assert W.rot_angle(a.pose[:3, :3] @ b.pose[:3, :3].T) < 1e-9 and np.abs(a.pose[:3, 3] - b.pose[:3, 3]).max() < 1e-9
+    assert a.n_corr == b.n_corr
 
 
 def test_run_c3(cil):

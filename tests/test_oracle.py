@@ -127,11 +127,15 @@ def test_golden_single_pair(oracle_lib, fname):
         np.testing.assert_array_equal(sys_.H, np.array(gd["H"]))
 
 
-def _residual_fd_jacobian(s, t, n, metric, h=1e-6):
+def _residual_fd_jacobian(s, t, n, metric, h=1e-6, w=(0.0, 0.0)):
     """Central finite differences of the TRUE residual r(x) of the rigidly moved point
-    s' = Rot(alpha) s + tau (scipy rotation), i.e. an independent construction of J."""
+    s' = Rot(alpha) s + tau (scipy rotation), i.e. an independent construction of J.
+    "combined" stacks the weighted residuals [sqrt(w_pp) (s'-t); sqrt(w_pl) (s'-t).n], whose
+    least-squares objective is w_pp |s'-t|^2 + w_pl ((s'-t).n)^2 (R22)."""
     def resid(x):
         sp = Rotation.from_rotvec(x[:3]).apply(s) + x[3:]
+        if metric == "combined":
+            return np.concatenate([np.sqrt(w[0]) * (sp - t), [np.sqrt(w[1]) * np.dot(sp - t, n)]])
         return np.atleast_1d(np.dot(sp - t, n)) if metric == "point_to_plane" else sp - t
     r0 = resid(np.zeros(6))
     J = np.zeros((r0.size, 6))
@@ -142,7 +146,7 @@ def _residual_fd_jacobian(s, t, n, metric, h=1e-6):
     return r0, J
 
 
-@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point", "combined"])
 def test_system_equals_finite_difference_jacobian(oracle_lib, metric):
     """H = sum J^T J, g = sum J^T r with J the derivative of the true residual (PAPER.md:140
     [Besl], [Low]).  A dropped term, wrong sign or transposed operand in the
@@ -156,11 +160,13 @@ def test_system_equals_finite_difference_jacobian(oracle_lib, metric):
     nrm = rng.standard_normal((m, 3))
     nrm = (nrm / np.linalg.norm(nrm, axis=1, keepdims=True)).astype(np.float32)
     # correspondences given explicitly (i <-> i) so that this pins only the accumulation
+    w = (0.3, 1.7)
+    oracle.set_combined_weights(*w)
     sys_ = oracle.icp_system_from_corr(tgt, nrm, src, pose, metric, np.arange(m, dtype=np.int32))
     Hs = np.zeros((6, 6))
     gs = np.zeros(6)
     for i in range(m):
-        r0, J = _residual_fd_jacobian(s[i], tgt[i].astype(np.float64), nrm[i].astype(np.float64), metric)
+        r0, J = _residual_fd_jacobian(s[i], tgt[i].astype(np.float64), nrm[i].astype(np.float64), metric, w=w)
         Hs += J.T @ J
         gs += J.T @ r0
     scale = np.abs(Hs).max()
@@ -405,3 +411,22 @@ def test_pca_normals_match_numpy_eigh(oracle_lib):
     np.testing.assert_allclose(curv, w[:, 0] / w.sum(1), atol=1e-6)
     # orientation toward the viewpoint (origin)
     assert (np.einsum("ni,ni->n", -pts.astype(np.float64), nrm.astype(np.float64)) >= -1e-7).all()
+
+
+@pytest.mark.parametrize("w", [(1.0, 0.0), (0.0, 1.0)])
+def test_combined_reduces_to_single_metrics(oracle_lib, w):
+    """SURVEY.md 8(f) NEXT-1 pin: weights (1,0) and (0,1) give the point-to-point and the
+    point-to-plane systems exactly (same correspondences, same ICP trajectory)."""
+    rng = np.random.default_rng(5)
+    tgt = rng.uniform(-1, 1, (400, 3)).astype(np.float32)
+    nrm = rng.standard_normal((400, 3))
+    nrm = (nrm / np.linalg.norm(nrm, axis=1, keepdims=True)).astype(np.float32)
+    src = (tgt + rng.normal(0, 0.01, tgt.shape)).astype(np.float32)
+    pose = _pose(Rotation.from_rotvec([0.02, 0.01, -0.03]).as_matrix(), np.array([0.01, -0.02, 0.0]))
+    oracle.set_combined_weights(*w)
+    single = "point_to_point" if w[0] == 1.0 else "point_to_plane"
+    a = oracle.icp_system(tgt, nrm, src, pose, "combined", 0.2)
+    b = oracle.icp_system(tgt, nrm, src, pose, single, 0.2)
+    np.testing.assert_array_equal(a.H, b.H)
+    np.testing.assert_array_equal(a.g, b.g)
+    assert a.sse == b.sse and a.count == b.count

@@ -190,6 +190,18 @@ cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const d
                        const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
                        double* iter_log, cil_stream_t stream);
 
+/* Surface normals of the TARGET points by PCA over their k nearest neighbours (SURVEY.md
+   8(f) NEXT-3; "normal estimation", PAPER.md:172-176 10-NN normals oriented
+   towards the viewpoint): for every target point p the exact k nearest targets (p itself
+   included; equal distances order by the lowest original index), their mean and 1/k
+   covariance (fp64), and the unit eigenvector of the smallest eigenvalue, flipped so that
+   n . (view - p) >= 0.  k in [3, 16].  view: HOST double[3] (NULL = the origin).
+   normals: device fp32 [n*3] in the target's original order; curvature (nullable): device
+   fp32 [n] = lambda_min / trace.  The result can be passed to cil_target_build as the
+   normals of a new target (the index itself is immutable). */
+cil_status cil_estimate_normals(const cil_target* t, int32_t k, const double* view, float* normals,
+                                float* curvature, cil_stream_t stream);
+
 /* Static strings; cil_last_error is thread-local detail for the last failing call. */
 const char* cil_status_string(cil_status s);
 const char* cil_last_error(void);

@@ -42,7 +42,7 @@ CIL_POINT_TO_PLANE = 1
 CIL_COMBINED = 2
 METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_PLANE, "combined": CIL_COMBINED}
 
-EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query",
+EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query", "cil_estimate_normals",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
             "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
             "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin"]
@@ -88,6 +88,8 @@ _lib.cil_target_get_info.restype = C.c_int
 _lib.cil_target_get_info.argtypes = [_vp, C.POINTER(cil_target_info)]
 _lib.cil_nn_query.restype = C.c_int
 _lib.cil_nn_query.argtypes = [_vp, _vp, _i64, C.c_float, _vp, _vp, _vp]
+_lib.cil_estimate_normals.restype = C.c_int
+_lib.cil_estimate_normals.argtypes = [_vp, C.c_int32, C.POINTER(C.c_double * 3), _vp, _vp, _vp]
 _lib.cil_icp_workspace_bytes.restype = _sz
 _lib.cil_icp_workspace_bytes.argtypes = [_i64, C.POINTER(cil_icp_params)]
 _lib.cil_icp_iterate.restype = C.c_int
@@ -262,6 +264,18 @@ def cil_nn_query(t: Target, queries: torch.Tensor, max_dist: float = math.inf, s
     _check(_lib.cil_nn_query(t.handle, _ptr(queries), m, float(max_dist), _ptr(idx), _ptr(sqdist),
                              _stream_ptr(stream)), "cil_nn_query")
     return idx, sqdist
+
+
+def cil_estimate_normals(t: Target, k: int = 10, view=(0.0, 0.0, 0.0), stream=None, want_curvature: bool = False,
+                         device="cuda"):
+    """PCA normals of the target over its k nearest neighbours, oriented towards `view`.
+    Returns (normals [n,3] fp32 device tensor in original order, curvature [n] or None)."""
+    nrm = torch.empty((t.n, 3), dtype=torch.float32, device=device)
+    cur = torch.empty(t.n, dtype=torch.float32, device=device) if want_curvature else None
+    v = (C.c_double * 3)(*[float(x) for x in view])
+    _check(_lib.cil_estimate_normals(t.handle, int(k), C.byref(v), _ptr(nrm), _ptr(cur), _stream_ptr(stream)),
+           "cil_estimate_normals")
+    return nrm, cur
 
 
 def cil_icp_workspace_bytes(m: int, params: cil_icp_params) -> int:

@@ -322,3 +322,51 @@ def test_icp_align_host_api(cil):
     o = oracle.icp_run(w.target, w.target_normals, w.source, "point_to_plane", 20, 0.1)
     assert W.rot_angle(res.pose[:3, :3] @ o.pose[:3, :3].T) <= 1e-4
     assert np.abs(res.pose[:3, 3] - o.pose[:3, 3]).max() <= 1e-5
+
+
+# ------------------------------------------------------------------ NEXT-3: PCA normals
+def _check_normals(cil, pts, k, view, min_gap=1e-3):
+    """cil_estimate_normals vs oracle.pca_normals: where the k-NN set is unambiguous (the k-th
+    and (k+1)-th fp64 distances differ by > 1e-6 relative) and the smallest eigenvalue is
+    separated (relative eigengap > min_gap), the normals agree to 1e-6 rad and the curvature to
+    1e-5 relative; everywhere the GPU normal is a unit vector facing the viewpoint."""
+    t = cil.cil_target_build(dev(pts), None)
+    g, gc = cil.cil_estimate_normals(t, k, view, want_curvature=True)
+    g, gc = g.cpu().numpy().astype(np.float64), gc.cpu().numpy().astype(np.float64)
+    o, oc = oracle.pca_normals(pts, k, view=view)
+    o = o.astype(np.float64)
+    tree = oracle.KDTree(pts)
+    idx, d2 = oracle.knn(None, pts.astype(np.float64), k=k + 1, tree=tree)
+    clear = (d2[:, k] - d2[:, k - 1]) > 1e-6 * np.maximum(d2[:, k - 1], 1e-300)
+    P = pts.astype(np.float64)[idx[:, :k]]
+    Cv = np.einsum("nki,nkj->nij", P - P.mean(1, keepdims=True), P - P.mean(1, keepdims=True)) / k
+    ev = np.linalg.eigvalsh(Cv)
+    sep = (ev[:, 1] - ev[:, 0]) > min_gap * np.maximum(ev[:, 2], 1e-300)
+    ok = clear & sep
+    assert ok.mean() > 0.9, ok.mean()
+    # angle from the cross product (arccos of a dot product near 1 is dominated by the fp32
+    # rounding of the normals' lengths); both normals renormalised in fp64
+    gn = g[ok] / np.linalg.norm(g[ok], axis=1, keepdims=True)
+    on = o[ok] / np.linalg.norm(o[ok], axis=1, keepdims=True)
+    ang = np.arcsin(np.clip(np.linalg.norm(np.cross(gn, on), axis=1), 0, 1))
+    assert ang.max() <= 1e-6, ang.max()
+    assert ((g[ok] * o[ok]).sum(1) > 0).all()                     # same orientation
+    np.testing.assert_allclose(gc[ok], oc[ok].astype(np.float64), rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(np.linalg.norm(g, axis=1), 1.0, atol=1e-6)
+    assert (((np.asarray(view) - pts.astype(np.float64)) * g).sum(1) >= -1e-6).all()
+    return ok.mean()
+
+
+@pytest.mark.parametrize("n,k", [(3000, 10), (20000, 6), (5000, 16)])
+def test_normals_random_surface(cil, n, k):
+    rng = np.random.default_rng(n + k)
+    u, v = rng.uniform(-1, 1, (2, n))
+    pts = np.stack([u, v, 0.2 * np.sin(2 * u) * np.cos(v)], 1) + rng.normal(0, 0.002, (n, 3))
+    _check_normals(cil, pts.astype(np.float32), k, (0.3, -0.2, 5.0))
+
+
+def test_normals_c3_config(cil):
+    """BASELINE.json configs[2]: the 640x480 depth frame, 10-NN, viewpoint at the camera."""
+    w = gen.c3_depth()
+    frac = _check_normals(cil, w.target, 10, (0.0, 0.0, 0.0))
+    assert frac > 0.95

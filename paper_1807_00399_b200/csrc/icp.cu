@@ -53,8 +53,10 @@ struct IterArgs {
     double* partials;        // [kMaxCtas * kSlots]
     IcpState* st;
     cil_icp_system* sys;     // iterate only, nullable
-    int32_t* corr_idx;       // iterate only, nullable
+    int32_t* corr_idx;       // iterate only, nullable (indexed by the caller's source order)
     float* corr_d2;          // iterate only, nullable
+    const uint32_t* perm;    // sorted slot -> caller's source index (the kernels run in Morton order)
+    float* srcs;             // [m*3] the source in Morton order (workspace)
     int* nn;                 // [m] match per query (original target index or -1)
     uint32_t* gw;            // [m] leaf-certificate word (run): bits(G1) & ~255 | anchor slot
     float* gs;               // [m] list-certificate margin G_S (run)
@@ -469,6 +471,7 @@ struct IcpQueries {
     uint32_t slot;
     int32_t* corr_idx;
     float* corr_d2;
+    const uint32_t* perm;
     __device__ __forceinline__ int packets(int m) const { return plist ? *(volatile const int*)plist_n : (m + 31) / 32; }
     __device__ __forceinline__ int tag() const { return (int)slot; }
     __device__ __forceinline__ int packet_base(int c) const { return 32 * (plist ? plist[c] : c); }
@@ -496,8 +499,9 @@ struct IcpQueries {
     __device__ __forceinline__ void store(int i, unsigned long long best, float) const {
         const bool found = best != bound_key(search2);
         nn[i] = found ? (int)key_idx(best) : -1;
-        if (corr_idx) corr_idx[i] = found ? (int32_t)key_idx(best) : -1;
-        if (corr_d2) corr_d2[i] = found ? key_d2(best) : INFINITY;
+        const size_t o = perm[i];                      // outputs in the caller's source order
+        if (corr_idx) corr_idx[o] = found ? (int32_t)key_idx(best) : -1;
+        if (corr_d2) corr_d2[o] = found ? key_d2(best) : INFINITY;
     }
     // CERT: the certificates of the new anchor (this iteration's pose).  G1 = d_out - d1 (leaf
     // form), G_S = r_S - d1 (candidate-leaf list); 4e-6 relative slack covers the fp32 d^2
@@ -573,6 +577,7 @@ icp_nn_kernel(const IterArgs a) {
     qs.slot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     qs.corr_idx = a.corr_idx;
     qs.corr_d2 = a.corr_d2;
+    qs.perm = a.perm;
     nn_packet_engine<B, CERT>(a.T, qs, a.m, &a.st->work);
 }
 
@@ -861,7 +866,7 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
 }
 
 struct WsLayout {
-    size_t state, partials, apose, adelta, nn, gw, pmask, plist, gs, gd1, gp, vlist, total;
+    size_t state, partials, apose, adelta, nn, gw, pmask, plist, gs, gd1, gp, vlist, perm, srcs, total;
 };
 
 WsLayout ws_layout(int64_t m) {
@@ -879,7 +884,9 @@ WsLayout ws_layout(int64_t m) {
     L.gd1 = L.gs + align_up(mm * sizeof(float), 256);
     L.gp = L.gd1 + align_up(mm * sizeof(float), 256);
     L.vlist = L.gp + align_up(mm * sizeof(uint32_t), 256);
-    L.total = L.vlist + align_up(mm * kListLeaves * sizeof(int), 256);
+    L.perm = L.vlist + align_up(mm * kListLeaves * sizeof(int), 256);
+    L.srcs = L.perm + align_up(mm * sizeof(uint32_t), 256);
+    L.total = L.srcs + align_up(mm * 3 * sizeof(float), 256);
     return L;
 }
 
@@ -897,7 +904,26 @@ void bind_ws(IterArgs& a, void* ws, int64_t m) {
     a.gs = (float*)(w + L.gs);
     a.gd1 = (float*)(w + L.gd1);
     a.gp = (uint32_t*)(w + L.gp);
+    a.perm = (const uint32_t*)(w + L.perm);
+    a.srcs = (float*)(w + L.srcs);
     a.vlist = (int*)(w + L.vlist);
+}
+
+__global__ void identity_perm_kernel(uint32_t* perm, int m) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) perm[k] = (uint32_t)k;
+}
+
+// The kernels visit the source in Morton order of its own frame (once per call; rigid motion
+// keeps the order spatially coherent), so a 32-query packet is a compact neighbourhood even
+// when the caller's order is not (C5's patch-major random samples).  a.src -> the sorted copy.
+cudaError_t sort_source(IterArgs& a, const float* src, cudaStream_t s) {
+    if (a.m == 0) { a.src = src; return cudaSuccess; }
+    if (debug_flags() & 16u) { a.src = src; identity_perm_kernel<<<std::max(1, std::min((a.m + 255) / 256, 4096)), 256, 0, s>>>(const_cast<uint32_t*>(a.perm), a.m); return cudaGetLastError(); }
+    int nl = 0;
+    cudaError_t e = morton_order_points(src, a.m, const_cast<uint32_t*>(a.perm), a.srcs, s, &nl);
+    count_launches(nl);
+    a.src = a.srcs;
+    return e;
 }
 
 cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
@@ -973,9 +999,11 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     a.run = 0;
     a.cert = 0;
     cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = sort_source(a, src, s);
+    if (e != cudaSuccess) return cuda_fail(e, "source Morton order");
     reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
     count_launches(1);
-    cudaError_t e = launch_iter(a, params->metric, s);
+    e = launch_iter(a, params->metric, s);
     if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
     return CIL_OK;
 }
@@ -1024,6 +1052,8 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.rot_tol = params->rot_tol;
     a.trans_tol = params->trans_tol;
     cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e0 = sort_source(a, src, s);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "source Morton order");
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
     run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, a.gp, (int)m, iter_log,
                                                 2 * params->max_iters);

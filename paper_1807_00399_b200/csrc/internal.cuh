@@ -93,6 +93,10 @@ void prof_end(cudaStream_t s);              // records the end event
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// target.cu: Morton order of a point set (perm: sorted position -> original index, sorted: the
+// points in that order, packed xyz); n >= 1
+cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* sorted, cudaStream_t s, int* nlaunch);
+
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);
 int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s);

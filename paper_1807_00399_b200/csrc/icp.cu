@@ -248,8 +248,8 @@ __device__ __forceinline__ float displacement_bound(const float* __restrict__ D,
 // a full search; K_nn then runs its packets in source order with only those lanes active, so
 // an uncertified remainder stays spatially coherent (a compacted list would scatter it).
 constexpr int kSelThreads = 256;
-constexpr int kSelRounds = 2;
-constexpr int kSelTile = kSelThreads * kSelRounds;     // 512 queries per CTA
+constexpr int kSelRounds = 4;
+constexpr int kSelTile = kSelThreads * kSelRounds;     // 1024 queries per CTA
 
 // Certificates of query i at the current pose, one query per lane, the
 // whole warp together: returns true if the lane's query needs a full search; otherwise its
@@ -267,6 +267,8 @@ struct SelWarp {
     unsigned long long best[32];
     unsigned sec[32];                        // point-level 2nd best (float bits)
     int items[32 * kListLeaves];
+    uint32_t rec[32 * kSelRounds];           // queued evaluations: index | leaf-certificate flag
+    float outer[32 * kSelRounds];            // their outer bounds
     int npc;                                 // point-certified queries (diagnostics)
 };
 
@@ -290,31 +292,51 @@ __device__ __forceinline__ void sel_leaf_item(const TargetView& T, const NegQuer
     if (v < *(volatile unsigned*)secS) atomicMin(secS, v);
 }
 
+// Phase 1 (per round of 32 points, one per lane): classify.  Points that need their leaf / list
+// evaluated are queued as records (index | leaf-certificate flag, outer bound) in the warp's
+// buffer, so that phase 2 evaluates them packed 32 per step instead of idling the lanes of
+// every round in which one point needs an evaluation.
+struct SelIn {                               // per-point state, loaded up front for every round
+    uint32_t w, wp;
+    int j;
+    float gs, gd1, px, py, pz;
+};
+
+__device__ __forceinline__ SelIn sel_load(const IterArgs& a, int i) {
+    SelIn v;
+    if (i < a.m) {
+        v.w = a.gw[i]; v.wp = a.gp[i]; v.j = a.nn[i]; v.gs = a.gs[i]; v.gd1 = a.gd1[i];
+        v.px = a.src[3 * (size_t)i]; v.py = a.src[3 * (size_t)i + 1]; v.pz = a.src[3 * (size_t)i + 2];
+    } else {
+        v.w = 0; v.wp = 0; v.j = -1; v.gs = 0.0f; v.gd1 = 0.0f; v.px = v.py = v.pz = 0.0f;
+    }
+    return v;
+}
+
 template <int B>
-__device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P, int i, uint32_t kslot, SelWarp& S) {
+__device__ __forceinline__ bool classify(const IterArgs& a, int i, const SelIn& in, uint32_t kslot, SelWarp& S,
+                                         int& nrec) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    bool need = false;
-    int nit = 0, j = -1;
+    bool need = false, eval = false;
+    uint32_t rec = 0;
     float outer = 0.0f;                      // lower bound of |s' - t| for every t outside the evaluated leaves
-    int4 l0 = make_int4(-1, -1, -1, -1), l1 = make_int4(-1, -1, -1, -1);
     if (i < a.m) {
-        const uint32_t w = a.gw[i];
-        const uint32_t wp = a.gp[i];
-        const float px = a.src[3 * (size_t)i], py = a.src[3 * (size_t)i + 1], pz = a.src[3 * (size_t)i + 2];
-        const float Gp = __uint_as_float(wp & ~255u);
+        const uint32_t w = in.w, wp = in.wp;
+        const float px = in.px, py = in.py, pz = in.pz;
         // slot == kslot: never anchored (iteration 0) or an anchor pose being recycled (k >= 256)
         if ((w & 255u) == kslot) {
             need = true;
         } else {
             const float D = displacement_bound(a.adelta + 16 * (w & 255u), px, py, pz);
             const float G1 = __uint_as_float(w & ~255u);
-            j = a.nn[i];
+            const int j = in.j;
             if (j < 0) {
                 need = !(G1 > D);
             } else {
                 const bool leaf_ok = G1 > 2.0f * D;
-                const float GS = leaf_ok ? 0.0f : a.gs[i];
+                const float GS = leaf_ok ? 0.0f : in.gs;
+                const float Gp = __uint_as_float(wp & ~255u);
                 if (!leaf_ok && !(GS > 2.0f * D)) {
                     need = true;
                 } else if (a.point_cert && (wp & 255u) != kslot && Gp > 0.0f &&
@@ -323,78 +345,104 @@ __device__ __forceinline__ bool certify_warp(const IterArgs& a, const Pose34& P,
                     // never postpones a search): nn[i] stays, nothing to evaluate
                     atomicAdd(&S.npc, 1);
                 } else {
-                    const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
-                    l0 = vl[0];
-                    if (!leaf_ok) l1 = vl[1];
-                    nit = leaf_ok ? 1
-                                  : (l0.x >= 0) + (l0.y >= 0) + (l0.z >= 0) + (l0.w >= 0) + (l1.x >= 0) +
-                                        (l1.y >= 0) + (l1.z >= 0) + (l1.w >= 0);
+                    eval = true;
+                    rec = (uint32_t)i | (leaf_ok ? 0x80000000u : 0u);
                     // targets outside the evaluated leaves were >= d_out (resp. r_S) from the anchor
-                    outer = (leaf_ok ? G1 : GS) + a.gd1[i] - D;
-                    const DF3 s = transform_df(P, px, py, pz);
-                    S.q[0][lane] = -s.hx; S.q[1][lane] = -s.hy; S.q[2][lane] = -s.hz;
-                    S.q[3][lane] = -s.lx; S.q[4][lane] = -s.ly; S.q[5][lane] = -s.lz;
-                    S.best[lane] = bound_key(INFINITY);
-                    S.sec[lane] = __float_as_uint(INFINITY);
+                    outer = (leaf_ok ? G1 : GS) + in.gd1 - D;
                 }
             }
         }
     }
-    // phase 1: L1 (entry 0) of every evaluating lane -- usually the winner; phase 2: the rest of
-    // the lists, flattened into rounds of 32 (query, leaf) items, each evaluated only if the
-    // leaf box can still beat the query's current best (else its bound joins the 2nd best)
-    NegQuery nq0;
-    if (nit > 0) {
-        nq0.hx = make_float2(S.q[0][lane], S.q[0][lane]); nq0.hy = make_float2(S.q[1][lane], S.q[1][lane]);
-        nq0.hz = make_float2(S.q[2][lane], S.q[2][lane]); nq0.lx = make_float2(S.q[3][lane], S.q[3][lane]);
-        nq0.ly = make_float2(S.q[4][lane], S.q[4][lane]); nq0.lz = make_float2(S.q[5][lane], S.q[5][lane]);
-        sel_leaf_item<B>(a.T, nq0, l0.x, &S.best[lane], &S.sec[lane]);
+    const unsigned mk = __ballot_sync(FULL, eval);
+    if (eval) {
+        const int pos = nrec + __popc(mk & ((1u << lane) - 1u));
+        S.rec[pos] = rec;
+        S.outer[pos] = outer;
     }
-    const int rest = nit > 1 ? nit - 1 : 0;
-    int incl = rest;
+    nrec += __popc(mk);
+    return need;
+}
+
+// Phase 2: the queued records, 32 per step: L1 (entry 0) of every record -- usually the winner
+// -- then the rest of the lists, flattened into rounds of 32 (query, leaf) items, each evaluated
+// only if the leaf box can still beat the query's current best (else its bound joins the 2nd
+// best); writes nn[i] and the re-measured point certificate.
+template <int B>
+__device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34& P, uint32_t kslot, SelWarp& S,
+                                                 int nrec) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    for (int c0 = 0; c0 < nrec; c0 += 32) {
+        const bool on = c0 + lane < nrec;
+        int i = 0, nit = 0;
+        float outer = 0.0f;
+        int4 l0 = make_int4(-1, -1, -1, -1), l1 = make_int4(-1, -1, -1, -1);
+        if (on) {
+            const uint32_t rec = S.rec[c0 + lane];
+            outer = S.outer[c0 + lane];
+            i = (int)(rec & 0x7fffffffu);
+            const bool leaf_ok = (rec >> 31) != 0;
+            const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
+            l0 = vl[0];
+            if (!leaf_ok) l1 = vl[1];
+            nit = leaf_ok ? 1
+                          : (l0.x >= 0) + (l0.y >= 0) + (l0.z >= 0) + (l0.w >= 0) + (l1.x >= 0) + (l1.y >= 0) +
+                                (l1.z >= 0) + (l1.w >= 0);
+            const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1], a.src[3 * (size_t)i + 2]);
+            S.q[0][lane] = -s.hx; S.q[1][lane] = -s.hy; S.q[2][lane] = -s.hz;
+            S.q[3][lane] = -s.lx; S.q[4][lane] = -s.ly; S.q[5][lane] = -s.lz;
+            S.best[lane] = bound_key(INFINITY);
+            S.sec[lane] = __float_as_uint(INFINITY);
+            NegQuery nq0;
+            nq0.hx = make_float2(-s.hx, -s.hx); nq0.hy = make_float2(-s.hy, -s.hy); nq0.hz = make_float2(-s.hz, -s.hz);
+            nq0.lx = make_float2(-s.lx, -s.lx); nq0.ly = make_float2(-s.ly, -s.ly); nq0.lz = make_float2(-s.lz, -s.lz);
+            sel_leaf_item<B>(a.T, nq0, l0.x, &S.best[lane], &S.sec[lane]);
+        }
+        const int rest = nit > 1 ? nit - 1 : 0;
+        int incl = rest;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(FULL, incl, 31);
-    if (total > 0) {
-        const int excl = incl - rest;
-        const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (total > 0) {
+            const int excl = incl - rest;
+            const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-        for (int c = 1; c < kListLeaves; ++c)
-            if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
-        __syncwarp();
-        for (int r0 = 0; r0 < total; r0 += 32) {
-            const int k = r0 + lane;
-            if (k < total) {
-                const int it = S.items[k];
-                const int q = it & 31;
-                NegQuery qq;
-                qq.hx = make_float2(S.q[0][q], S.q[0][q]);
-                qq.hy = make_float2(S.q[1][q], S.q[1][q]);
-                qq.hz = make_float2(S.q[2][q], S.q[2][q]);
-                qq.lx = make_float2(S.q[3][q], S.q[3][q]);
-                qq.ly = make_float2(S.q[4][q], S.q[4][q]);
-                qq.lz = make_float2(S.q[5][q], S.q[5][q]);
-                const float lb = leaf_lb2(a.T, qq, it >> 5);
-                if (lb <= key_d2(*(volatile unsigned long long*)&S.best[q])) sel_leaf_item<B>(a.T, qq, it >> 5, &S.best[q], &S.sec[q]);
-                else atomicMin(&S.sec[q], __float_as_uint(lb));
+            for (int c = 1; c < kListLeaves; ++c)
+                if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
+            __syncwarp();
+            for (int r0 = 0; r0 < total; r0 += 32) {
+                const int k = r0 + lane;
+                if (k < total) {
+                    const int it = S.items[k];
+                    const int q = it & 31;
+                    NegQuery qq;
+                    qq.hx = make_float2(S.q[0][q], S.q[0][q]);
+                    qq.hy = make_float2(S.q[1][q], S.q[1][q]);
+                    qq.hz = make_float2(S.q[2][q], S.q[2][q]);
+                    qq.lx = make_float2(S.q[3][q], S.q[3][q]);
+                    qq.ly = make_float2(S.q[4][q], S.q[4][q]);
+                    qq.lz = make_float2(S.q[5][q], S.q[5][q]);
+                    const float lb = leaf_lb2(a.T, qq, it >> 5);
+                    if (lb <= key_d2(*(volatile unsigned long long*)&S.best[q])) sel_leaf_item<B>(a.T, qq, it >> 5, &S.best[q], &S.sec[q]);
+                    else atomicMin(&S.sec[q], __float_as_uint(lb));
+                }
             }
         }
+        __syncwarp();
+        if (on) {
+            const unsigned long long b = S.best[lane];
+            const int jn = (int)key_idx(b);
+            if (jn != a.nn[i]) a.nn[i] = jn;
+            // point certificate measured here: every other target is at >= min(2nd best, outer)
+            const float o2 = fminf(sqrtf(__uint_as_float(S.sec[lane])), outer);
+            const float Gp = fmaxf(o2 * (1.0f - 4e-6f) - sqrtf(key_d2(b)) * (1.0f + 4e-6f), 0.0f);
+            a.gp[i] = (__float_as_uint(Gp) & ~255u) | kslot;
+        }
+        __syncwarp();
     }
-    __syncwarp();
-    if (nit > 0) {
-        const unsigned long long b = S.best[lane];
-        const int jn = (int)key_idx(b);
-        if (jn != j) a.nn[i] = jn;
-        // point certificate measured here: every other target is at >= min(2nd best, outer)
-        const float o2 = fminf(sqrtf(__uint_as_float(S.sec[lane])), outer);
-        const float Gp = fmaxf(o2 * (1.0f - 4e-6f) - sqrtf(key_d2(b)) * (1.0f + 4e-6f), 0.0f);
-        a.gp[i] = (__float_as_uint(Gp) & ~255u) | kslot;
-    }
-    __syncwarp();
-    return need;
 }
 
 template <int B>
@@ -416,18 +464,23 @@ icp_select_kernel(const IterArgs a) {
 #pragma unroll
     for (int e = 0; e < 12; ++e) P.r[e] = s_pose[e];
     const int wbase = blockIdx.x * kSelTile + warp * (32 * kSelRounds);
-    int cnt = 0;
+    int cnt = 0, nrec = 0;
+    SelIn in[kSelRounds];                    // every round's loads in flight together
+#pragma unroll
+    for (int r = 0; r < kSelRounds; ++r) in[r] = sel_load(a, wbase + 32 * r + lane);
 #pragma unroll
     for (int r = 0; r < kSelRounds; ++r) {
         const int i0 = wbase + 32 * r;
         if (i0 >= a.m) break;
-        const unsigned mk = __ballot_sync(FULL, certify_warp<B>(a, P, i0 + lane, kslot, s_w[warp]));
+        const unsigned mk = __ballot_sync(FULL, classify<B>(a, i0 + lane, in[r], kslot, s_w[warp], nrec));
         if (lane == 0) {
             a.pmask[i0 >> 5] = mk;
             if (mk) s_pk[atomicAdd(&s_np, 1)] = i0 >> 5;
         }
         cnt += __popc(mk);
     }
+    __syncwarp();
+    evaluate_records<B>(a, P, kslot, s_w[warp], nrec);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
     // packets that need a search go to the list (one global atomic per CTA; any order: a

@@ -457,6 +457,44 @@ __device__ __forceinline__ int key_bound(const TargetView& T, unsigned long long
     return lo;
 }
 
+// Warp-cooperative bounds of the sorted key range [first key >= clo, first key > chi): each
+// half-warp runs a 16-ary search (16 pivots split the bracket into 17 segments per step) inside
+// the coarse cell of its code, so a bracket of n keys takes ~log17(n) dependent loads.
+__device__ __forceinline__ void key_range_warp(const TargetView& T, unsigned long long clo, unsigned long long chi,
+                                               int& i0, int& i1) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15;
+    const bool upper = h != 0;
+    const unsigned long long code = upper ? chi : clo;
+    const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
+    int lo = (int)__ldg(T.cell_first + c), hi = (int)__ldg(T.cell_first + c + 1);   // answer in [lo, hi]
+    while (true) {
+        const int n = hi - lo;
+        if (!__any_sync(FULL, n > 0)) break;
+        int idx;
+        if (n <= 16) idx = lo + l;
+        else idx = lo + (int)(((long long)(l + 1) * n) / 17);
+        bool pred = false;
+        if (n > 0 && idx < hi) {
+            const unsigned long long k = __ldg(T.keys + idx);
+            pred = upper ? k <= code : k < code;
+        }
+        const unsigned t = __popc((__ballot_sync(FULL, pred) >> (16 * h)) & 0xffffu);
+        if (n > 0) {
+            if (n <= 16) {
+                lo = hi = lo + (int)t;
+            } else {
+                const int a = t == 0 ? lo : lo + (int)(((long long)t * n) / 17) + 1;
+                const int b = t == 16 ? hi : lo + (int)(((long long)(t + 1) * n) / 17);
+                lo = a;
+                hi = b;
+            }
+        }
+    }
+    i0 = __shfl_sync(FULL, lo, 0);
+    i1 = __shfl_sync(FULL, lo, 16);
+}
+
 template <int B, bool CERT, class Q>
 __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int m, unsigned int* counter) {
     const unsigned FULL = 0xffffffffu;
@@ -604,18 +642,15 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             int* F = sF[wid][0];
             int* G = sF[wid][1];
             // ---- C: Morton range of P -> leaf range -> candidate leaves (node ids)
-            // (bracketed by the coarse-cell table: [first of code(P.lo)'s cell, first after
-            // code(P.hi)'s cell) is a superset of the key range -- two independent loads
-            // instead of a chain of binary-search steps)
-            int ib = 0;
-            if (lane < 2) {
+            // (exact bounds by a warp-cooperative 16-ary search: lanes 0-15 find the first key
+            // >= code(P.lo), lanes 16-31 the first key > code(P.hi), inside the coarse cells)
+            int i0, i1;
+            {
                 const float4 Qz = __ldg(T.quant);
-                const unsigned long long code = lane == 0 ? morton_of(Qz, plo.x, plo.y, plo.z)
-                                                          : morton_of(Qz, phi.x, phi.y, phi.z);
-                const unsigned c = (unsigned)(code >> (3 * kMortonBits - T.coarse_bits));
-                ib = (int)__ldg(T.cell_first + c + (lane == 1 ? 1u : 0u));
+                const unsigned long long clo = morton_of(Qz, plo.x, plo.y, plo.z);
+                const unsigned long long chi = morton_of(Qz, phi.x, phi.y, phi.z);
+                key_range_warp(T, clo, chi, i0, i1);
             }
-            const int i0 = __shfl_sync(FULL, ib, 0), i1 = __shfl_sync(FULL, ib, 1);
             int nF = 0;
             dbg_i0 = i0; dbg_i1 = i1;
             if (i1 > i0) {

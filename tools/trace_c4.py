@@ -56,7 +56,7 @@ for k in (2, 10, 30):
     summarize(f"run (no cert) iteration {k}", tr.cpu().numpy().reshape(-1, 16))
 
 cil.set_certificates(True)
-for k in (40,):
+for k in (6, 40):
     pk = cil.make_params(metric, k, 1.0)
     ws = cil.alloc_workspace(w.m, pk)
     tr[:] = 0
@@ -65,7 +65,7 @@ for k in (40,):
     torch.cuda.synchronize()
     cil.lib().cil_debug_engine_trace(None)
     a = tr.cpu().numpy().reshape(-1, 16)
-    for it in (k - 3, k - 2, k - 1):
+    for it in ((k - 1,) if k < 10 else (k - 3, k - 2, k - 1)):
         sel = (a[:, 8] != 0) & (a[:, 13] == it)
         r = a[sel]
         if len(r) == 0:

@@ -611,15 +611,23 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         bool normal = active && r <= rcap && r < INFINITY;
         if (T.dbg_mode == 1) normal = false;
         if (T.dbg_mode == 2) normal = active && r < INFINITY;
+        // an outlier (radius above the cap) joins the packet with its ball capped at rcap: if its
+        // nearest neighbour lies within the cap the packet phases find it exactly, otherwise it
+        // finishes with the ballot DFS
         const bool outlier = active && !normal;
+        const bool capped = outlier && r < INFINITY && T.dbg_mode == 0;
+        const float rcap2 = rcap * rcap;
+        if (CERT && capped) sThr[wid][lane] = fminf(thr, rcap2);     // list appends stop at the cap
+        const bool inP = normal || capped;
+        const float rP = normal ? r : rcap;
         // inflate for the double-float offset and for rounding of s_hi -/+ r
-        const float rx = r * 1.000001f + fabsf(s.lx) + 1e-6f * fabsf(s.hx) + 1e-30f;
-        const float ry = r * 1.000001f + fabsf(s.ly) + 1e-6f * fabsf(s.hy) + 1e-30f;
-        const float rz = r * 1.000001f + fabsf(s.lz) + 1e-6f * fabsf(s.hz) + 1e-30f;
-        float4 plo = make_float4(normal ? s.hx - rx : INFINITY, normal ? s.hy - ry : INFINITY,
-                                 normal ? s.hz - rz : INFINITY, 0.0f);
-        float4 phi = make_float4(normal ? s.hx + rx : -INFINITY, normal ? s.hy + ry : -INFINITY,
-                                 normal ? s.hz + rz : -INFINITY, 0.0f);
+        const float rx = rP * 1.000001f + fabsf(s.lx) + 1e-6f * fabsf(s.hx) + 1e-30f;
+        const float ry = rP * 1.000001f + fabsf(s.ly) + 1e-6f * fabsf(s.hy) + 1e-30f;
+        const float rz = rP * 1.000001f + fabsf(s.lz) + 1e-6f * fabsf(s.hz) + 1e-30f;
+        float4 plo = make_float4(inP ? s.hx - rx : INFINITY, inP ? s.hy - ry : INFINITY,
+                                 inP ? s.hz - rz : INFINITY, 0.0f);
+        float4 phi = make_float4(inP ? s.hx + rx : -INFINITY, inP ? s.hy + ry : -INFINITY,
+                                 inP ? s.hz + rz : -INFINITY, 0.0f);
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             plo.x = fminf(plo.x, __shfl_xor_sync(FULL, plo.x, o));
@@ -631,14 +639,14 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         }
         // sparse packet (the balls fill a small part of P: e.g. an uncertified remainder
         // spread along the scan): every lane searches on its own
-        float vb = normal ? 8.0f * rx * ry * rz : 0.0f;
+        float vb = inP ? 8.0f * rx * ry * rz : 0.0f;
 #pragma unroll
         for (int o = 16; o; o >>= 1) vb += __shfl_xor_sync(FULL, vb, o);
         const bool sparse = (phi.x - plo.x) * (phi.y - plo.y) * (phi.z - plo.z) > 32.0f * vb;
         if (tracing) ckB = (unsigned)clock();
         bool overflow = false;
         int dbg_i0 = -1, dbg_i1 = -1, dbg_nF = -1, dbg_items = 0;
-        if (!sparse && __any_sync(FULL, normal)) {
+        if (!sparse && __any_sync(FULL, inP)) {
             int* F = sF[wid][0];
             int* G = sF[wid][1];
             // ---- C: Morton range of P -> leaf range -> candidate leaves (node ids)
@@ -748,7 +756,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                     best = sBest[wid][lane];
                     if (CERT) sec = __uint_as_float(sSec[wid][lane]);
                     if (active) thr = thr_of(best);
-                    if (CERT) sThr[wid][lane] = thr;
+                    if (CERT) sThr[wid][lane] = capped ? fminf(thr, rcap2) : thr;
                 };
                 // four candidate leaves per step: their box loads are in flight together
                 for (int k = 0; k < nF; k += 4) {
@@ -760,7 +768,8 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                     for (int u = 0; u < 4; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, nq, f[u]) : INFINITY;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const bool need = normal && f[u] >= 0 && f[u] != hint && f[u] != hint2 && lb[u] <= thr;
+                        const bool need = inP && f[u] >= 0 && f[u] != hint && f[u] != hint2 &&
+                                          lb[u] <= (capped ? fminf(thr, rcap2) : thr);
                         const unsigned mk = __ballot_sync(FULL, need);
                         if (need) items[nI + __popc(mk & lt)] = (f[u] << 5) | lane;
                         nI += __popc(mk);
@@ -784,9 +793,12 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             rec[14] = __popc(__ballot_sync(__activemask(), active));
         }
         // ---- F: exact ballot DFS for outliers (or everyone after an overflow)
+        // a capped lane whose match lies within its cap is done (every leaf reaching into the
+        // cap ball was examined); its certificate bookkeeping stops at the cap
+        const bool cap_done = capped && !sparse && !overflow && key_d2(best) <= rcap2;
         // sparse packet: independent per-lane DFS; outliers / overflow: ballot DFS
-        const bool lane_on = sparse && normal;
-        const bool ballot_on = outlier || (overflow && normal);
+        const bool lane_on = sparse && inP;
+        const bool ballot_on = (outlier && !cap_done && !(sparse && capped)) || (overflow && inP);
         {
             unsigned drop = 0u;
             int cnt = 0;
@@ -805,11 +817,12 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         if (active) {
             // targets outside the evaluated leaves are beyond the final threshold
             const bool cert_ok = CERT;
-            const float lb_out2 = cert_ok ? fminf(sec, thr) : 0.0f;
+            const float thr_done = cap_done ? fminf(thr, rcap2) : thr;   // what was examined
+            const float lb_out2 = cert_ok ? fminf(sec, thr_done) : 0.0f;
             if constexpr (CERT) {
                 // candidate-leaf list: every target outside it is beyond min(thr, drop)
                 const int cnt = cert_ok ? min(sCnt[wid][lane], kListLeaves) : 0;
-                const float rS2 = fminf(thr, __uint_as_float(sDrop[wid][lane]));
+                const float rS2 = fminf(thr_done, __uint_as_float(sDrop[wid][lane]));
                 qs.store(qi, best, lb_out2, sList[wid][lane], cnt, rS2);
             } else {
                 qs.store(qi, best, lb_out2);

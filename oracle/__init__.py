@@ -11,6 +11,9 @@ Parity status of each function:
   solve_update ............ pinned (numpy.linalg.solve, scipy Rotation.from_rotvec)
   icp_run ................. pinned (Kabsch/SVD fixed point, planted-motion recovery,
                              translation-only closed form, equivariance)
+  proj_system / proj_run .. pinned (identity self-pairing, one-pixel shift closed form,
+                             half-away-from-zero rounding, bounds/invalid/rejection cases,
+                             accumulation = icp_system_from_corr on the same pairs)
   pca_normals ............. pinned (noise-free planes, numpy eigh on explicit neighbourhoods)
 """
 from __future__ import annotations
@@ -76,6 +79,14 @@ def lib():
                                   C.c_double, C.c_double, C.c_double, _f64p, C.POINTER(C.c_double),
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32), _opt(_f64p), _opt(_f64p), _opt(_f64p), _opt(_f64p)]
+        L.orc_proj_system.argtypes = [_f32p, _opt(_f32p), C.c_int64, C.c_int64, _f64p, _f32p, C.c_int64, _f64p,
+                                      C.c_int, C.c_double, _f64p, _f64p, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64), _opt(_f64p), _opt(_f64p), _opt(_i64p), _opt(_f64p),
+                                      _opt(_f64p)]
+        L.orc_proj_run.argtypes = [_f32p, _opt(_f32p), C.c_int64, C.c_int64, _f64p, _f32p, C.c_int64, _f64p, C.c_int,
+                                   C.c_int, C.c_double, C.c_double, C.c_double, _f64p, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32), _opt(_f64p), _opt(_f64p), _opt(_f64p), _opt(_f64p)]
         L.orc_pca_normals.argtypes = [C.c_void_p, _f32p, C.c_int64, C.c_int, _f64p, _f32p, _opt(_f32p)]
         _lib = L
     return _lib
@@ -239,6 +250,59 @@ def icp_run(target, normals, source, metric: str, max_iters: int, max_dist: floa
     return RunResult(pose.reshape(4, 4), rmse.value, nc.value, n_it, bool(cv.value), st.value,
                      log.reshape(K, 2)[:n_it], Hl.reshape(K, 6, 6)[:n_it], gl.reshape(K, 6)[:n_it],
                      Pl.reshape(K, 4, 4)[:n_it])
+
+
+@dataclass
+class ProjSystem(System):
+    uv: np.ndarray | None = None
+
+
+def _intr(intr) -> np.ndarray:
+    """intr = (width, height, fx, fy, cx, cy) -> (w, h, [fx, fy, cx, cy])"""
+    w, h, fx, fy, cx, cy = intr
+    return int(w), int(h), np.array([fx, fy, cx, cy], np.float64)
+
+
+def proj_system(target, normals, intr, source, pose, metric: str, max_dist: float) -> ProjSystem:
+    """projective correspondences (DESIGN.md R23-R26) + the normal equations of one iteration;
+    target: organised [w*h, 3] in row-major pixel order"""
+    tgt = _pts(target)
+    nrm = None if normals is None else _pts(normals)
+    src = _pts(source)
+    w, h, K = _intr(intr)
+    assert tgt.shape[0] == w * h
+    m = src.shape[0]
+    H = np.zeros(36); g = np.zeros(6); Ha = np.zeros(36); ga = np.zeros(6)
+    sse = C.c_double(); cnt = C.c_int64()
+    ci = np.empty(m, np.int64); cd = np.empty(m, np.float64); uv = np.empty(2 * m, np.float64)
+    rc = lib().orc_proj_system(tgt, nrm, w, h, K, src, m, np.ascontiguousarray(pose, np.float64).reshape(16),
+                               METRICS[metric], float(max_dist), H, g, C.byref(sse), C.byref(cnt), Ha, ga, ci, cd, uv)
+    if rc:
+        raise ValueError(f"orc_proj_system rc={rc}")
+    return ProjSystem(H.reshape(6, 6), g, sse.value, cnt.value, Ha.reshape(6, 6), ga, ci, cd, None, uv.reshape(m, 2))
+
+
+def proj_run(target, normals, intr, source, metric: str, max_iters: int, max_dist: float, pose_init=None,
+             rot_tol: float = 0.0, trans_tol: float = 0.0) -> RunResult:
+    tgt = _pts(target)
+    nrm = None if normals is None else _pts(normals)
+    src = _pts(source)
+    w, h, K = _intr(intr)
+    assert tgt.shape[0] == w * h
+    P0 = np.eye(4) if pose_init is None else np.asarray(pose_init, np.float64)
+    pose = np.empty(16); rmse = C.c_double(); nc = C.c_int64()
+    it = C.c_int32(); cv = C.c_int32(); st = C.c_int32()
+    n = max(int(max_iters), 1)
+    log = np.zeros(2 * n); Hl = np.zeros(36 * n); gl = np.zeros(6 * n); Pl = np.zeros(16 * n)
+    rc = lib().orc_proj_run(tgt, nrm, w, h, K, src, src.shape[0], np.ascontiguousarray(P0).reshape(16),
+                            METRICS[metric], int(max_iters), float(max_dist), float(rot_tol), float(trans_tol),
+                            pose, C.byref(rmse), C.byref(nc), C.byref(it), C.byref(cv), C.byref(st), log, Hl, gl, Pl)
+    if rc:
+        raise ValueError(f"orc_proj_run rc={rc}")
+    n_it = it.value
+    return RunResult(pose.reshape(4, 4), rmse.value, nc.value, n_it, bool(cv.value), st.value,
+                     log.reshape(n, 2)[:n_it], Hl.reshape(n, 6, 6)[:n_it], gl.reshape(n, 6)[:n_it],
+                     Pl.reshape(n, 4, 4)[:n_it])
 
 
 def pca_normals(pts, k: int = 10, view=(0.0, 0.0, 0.0), tree: KDTree | None = None, brute: bool = False):

@@ -26,6 +26,9 @@
  *     R <- exp([alpha]x) R, t <- exp([alpha]x) t + tau (R5).
  *   - the ICP loop ("alternating between correspondence estimation and
  *     transformation parameter optimization", PAPER.md:195 fixed iteration count).
+ *   - projective data association for organised clouds (
+ *     SPEC.md:392-400): project s through the target intrinsics, round half away from
+ *     zero, take that pixel's point if valid and within max_dist.
  *   - PCA normals over k-NN (used only to build config-3 inputs, as
  *     BASELINE.json configs[2] asks for "normals from oracle PCA over 10-NN").
  *
@@ -481,24 +484,91 @@ int orc_solve_update(const double H[36], const double g[6], int64_t count, const
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------ projective association */
+/* The second correspondence engine of the paper: projective data association for organised
+   3-D clouds ("different correspondence search engines (e.g., kd-tree based or
+   projective)", "one for correspondences by projective data association for the
+   3D case"; SPEC.md:392-400 correspondences_projective; pixel rounding SPEC.md:117; DESIGN.md
+   readings R23-R26).
+   The target is organised: tgt[3 * (v * w + u)] is the point of pixel (u, v) in the target
+   camera frame; a pixel is invalid when its z <= 0 or a coordinate is not finite.
+   intr = {fx, fy, cx, cy}.  For source point p: s = R p + t; if s_z > 0 then
+   u = round(fx * s_x / s_z + cx), v = round(fy * s_y / s_z + cy) with C round() (half away
+   from zero); the pair (i, v * w + u) exists iff 0 <= u < w, 0 <= v < h, the pixel is valid
+   and |s - t|^2 <= max_dist^2 (inclusive, as R2).
+   Returns the pixel index or -1; *d2 = |s - t|^2 of an accepted pair, else +inf; uv (nullable)
+   = the unrounded (u, v), NaN when s_z <= 0 (tests use it for the rounding band R24). */
+static int64_t proj_one(const float* tgt, int64_t w, int64_t h, const double intr[4], const double s[3],
+                        double bound2, double* d2, double* uv) {
+    *d2 = INFINITY;
+    if (uv) { uv[0] = NAN; uv[1] = NAN; }
+    if (!(s[2] > 0.0)) return -1;
+    double uf = intr[0] * s[0] / s[2] + intr[2];
+    double vf = intr[1] * s[1] / s[2] + intr[3];
+    if (uv) { uv[0] = uf; uv[1] = vf; }
+    double ur = round(uf), vr = round(vf);
+    if (!(ur >= 0.0 && ur < (double)w && vr >= 0.0 && vr < (double)h)) return -1;
+    int64_t k = (int64_t)vr * w + (int64_t)ur;
+    const float* t = tgt + 3 * k;
+    if (!(t[2] > 0.0f) || !isfinite(t[0]) || !isfinite(t[1]) || !isfinite(t[2])) return -1;
+    double e = dist2(s, t);
+    if (!(e <= bound2)) return -1;
+    *d2 = e;
+    return k;
+}
+
+/* One projective correspondence + normal-equation pass (a1, projective a2, a3-a5), the
+   accumulation serial in source-index order exactly as orc_icp_system. */
+int orc_proj_system(const float* tgt, const float* nrm, int64_t w, int64_t h, const double intr[4],
+                    const float* src, int64_t m, const double pose[16], int metric, double max_dist,
+                    double H[36], double g[6], double* sse, int64_t* count, double* Habs, double* gabs,
+                    int64_t* corr_idx, double* corr_d2, double* uv) {
+    if ((metric == MET_P2PLANE || metric == MET_COMBINED) && !nrm) return 3;
+    if (w < 1 || h < 1) return 1;
+    double bound2 = max_dist * max_dist;
+    memset(H, 0, 36 * sizeof(double));
+    memset(g, 0, 6 * sizeof(double));
+    if (Habs) memset(Habs, 0, 36 * sizeof(double));
+    if (gabs) memset(gabs, 0, 6 * sizeof(double));
+    *sse = 0.0;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        double s[3], d2;
+        transform_point(pose, src + 3 * i, s);
+        int64_t k = proj_one(tgt, w, h, intr, s, bound2, &d2, uv ? uv + 2 * i : NULL);
+        if (corr_idx) corr_idx[i] = k;
+        if (corr_d2) corr_d2[i] = d2;
+        if (k < 0) continue;
+        add_pair(metric, s, tgt + 3 * k, nrm ? nrm + 3 * k : NULL, H, g, sse, Habs, gabs);
+        ++cnt;
+    }
+    *count = cnt;
+    return 0;
+}
+
 /* ------------------------------------------------------------------ ICP loop */
 /* iter_log (nullable) [max_iters*2] = {n_corr, rmse}; H_log [max_iters*36], g_log [max_iters*6]
    (nullable) record each executed iteration's system; pose_log [max_iters*16] the pose
    after each executed iteration. */
-int orc_icp_run(const void* kd, const float* tgt, const float* nrm, int64_t n,
-                const float* src, int64_t m, const double pose_init[16], int metric, int max_iters,
-                double max_dist, double rot_tol, double trans_tol,
-                double pose_out[16], double* rmse, int64_t* n_corr, int32_t* iterations,
-                int32_t* converged, int32_t* status,
-                double* iter_log, double* H_log, double* g_log, double* pose_log) {
+/* engine 0: exact NN (kd or brute force); engine 1: projective (w, h, intr) */
+static int icp_loop(int engine, const void* kd, const float* tgt, const float* nrm, int64_t n,
+                    int64_t w, int64_t h, const double* intr,
+                    const float* src, int64_t m, const double pose_init[16], int metric, int max_iters,
+                    double max_dist, double rot_tol, double trans_tol,
+                    double pose_out[16], double* rmse, int64_t* n_corr, int32_t* iterations,
+                    int32_t* converged, int32_t* status,
+                    double* iter_log, double* H_log, double* g_log, double* pose_log) {
     double P[16];
     memcpy(P, pose_init, sizeof(P));
     *rmse = 0.0; *n_corr = 0; *iterations = 0; *converged = 0; *status = ORC_OK;
     for (int it = 0; it < max_iters; ++it) {
         double H[36], g[6], sse, x[6], th, tn;
         int64_t cnt;
-        int rc = orc_icp_system(kd, tgt, nrm, n, src, m, P, metric, max_dist, H, g, &sse, &cnt,
-                                NULL, NULL, NULL, NULL, NULL);
+        int rc = engine == 0
+                     ? orc_icp_system(kd, tgt, nrm, n, src, m, P, metric, max_dist, H, g, &sse, &cnt,
+                                      NULL, NULL, NULL, NULL, NULL)
+                     : orc_proj_system(tgt, nrm, w, h, intr, src, m, P, metric, max_dist, H, g, &sse, &cnt,
+                                       NULL, NULL, NULL, NULL, NULL);
         if (rc) return rc;
         *iterations = it + 1;
         double r = cnt > 0 ? sqrt(sse / (double)cnt) : 0.0;
@@ -514,6 +584,28 @@ int orc_icp_run(const void* kd, const float* tgt, const float* nrm, int64_t n,
     }
     memcpy(pose_out, P, sizeof(P));
     return 0;
+}
+
+int orc_icp_run(const void* kd, const float* tgt, const float* nrm, int64_t n,
+                const float* src, int64_t m, const double pose_init[16], int metric, int max_iters,
+                double max_dist, double rot_tol, double trans_tol,
+                double pose_out[16], double* rmse, int64_t* n_corr, int32_t* iterations,
+                int32_t* converged, int32_t* status,
+                double* iter_log, double* H_log, double* g_log, double* pose_log) {
+    return icp_loop(0, kd, tgt, nrm, n, 0, 0, NULL, src, m, pose_init, metric, max_iters, max_dist, rot_tol,
+                    trans_tol, pose_out, rmse, n_corr, iterations, converged, status, iter_log, H_log, g_log, pose_log);
+}
+
+/* the ICP loop with projective correspondences (the same solve/update and stop rules) */
+int orc_proj_run(const float* tgt, const float* nrm, int64_t w, int64_t h, const double intr[4],
+                 const float* src, int64_t m, const double pose_init[16], int metric, int max_iters,
+                 double max_dist, double rot_tol, double trans_tol,
+                 double pose_out[16], double* rmse, int64_t* n_corr, int32_t* iterations,
+                 int32_t* converged, int32_t* status,
+                 double* iter_log, double* H_log, double* g_log, double* pose_log) {
+    if (w < 1 || h < 1) return 1;
+    return icp_loop(1, NULL, tgt, nrm, w * h, w, h, intr, src, m, pose_init, metric, max_iters, max_dist, rot_tol,
+                    trans_tol, pose_out, rmse, n_corr, iterations, converged, status, iter_log, H_log, g_log, pose_log);
 }
 
 /* ------------------------------------------------------------------ PCA normals */

@@ -202,6 +202,36 @@ cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const d
 cil_status cil_estimate_normals(const cil_target* t, int32_t k, const double* view, float* normals,
                                 float* curvature, cil_stream_t stream);
 
+/* ---- Projective data association ----
+   The paper's second correspondence engine: PAPER.md:83 ("different correspondence search
+   engines (e.g., kd-tree based or projective)"), PAPER.md:140 ("one for correspondences by
+   projective data association for the 3D case"); R23-R26.
+   The target is an ORGANISED cloud: width*height points, packed fp32 xyz, row-major pixels
+   (pixel (u, v) = point v*width + u) in the target camera frame; a pixel is invalid when its
+   z <= 0 or a coordinate is not finite.  Source point p maps to s = R p + t (fp64) and
+   projects to u = round(fx s_x / s_z + cx), v = round(fy s_y / s_z + cy), evaluated in fp64
+   as ((f s) / s_z) + c and rounded half away from zero.  The pair
+   (i, v*width + u) exists iff s_z > 0, 0 <= u < width, 0 <= v < height, the pixel is valid
+   and |s - t| <= max_corr_dist (inclusive).  Steps a3-a7 are those of cil_icp_iterate.
+   intrinsics: HOST struct, width, height >= 1, width*height <= INT32_MAX, fx, fy > 0 finite,
+   cx, cy finite.  tgt / tgt_normals (nullable for point-to-point): device fp32 [w*h*3],
+   caller-owned, read only (no index is built: the image IS the index).  The workspace is
+   O(1) (cil_proj_workspace_bytes, independent of m); everything else as cil_icp_iterate /
+   cil_icp_run (corr_idx = pixel index or -1). */
+typedef struct {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+} cil_intrinsics;
+
+size_t cil_proj_workspace_bytes(int64_t m, const cil_icp_params* params);
+cil_status cil_proj_iterate(const float* tgt, const float* tgt_normals, const cil_intrinsics* intrinsics,
+                            const float* src, int64_t m, const double* pose_in, const cil_icp_params* params,
+                            void* ws, size_t ws_bytes, double* pose_out, cil_icp_system* sys, int32_t* corr_idx,
+                            float* corr_sqdist, cil_stream_t stream);
+cil_status cil_proj_run(const float* tgt, const float* tgt_normals, const cil_intrinsics* intrinsics,
+                        const float* src, int64_t m, const double* pose_init, const cil_icp_params* params,
+                        void* ws, size_t ws_bytes, cil_icp_result* res, double* iter_log, cil_stream_t stream);
+
 /* Static strings; cil_last_error is thread-local detail for the last failing call. */
 const char* cil_status_string(cil_status s);
 const char* cil_last_error(void);
@@ -244,6 +274,14 @@ cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kapp
    phases, work items, final best d2, SM clocks of phases A, B, C, D+E, F, 0, 0, 0}.  NULL
    switches it off.  Host-only, process-wide. */
 cil_status cil_debug_engine_trace(int32_t* buf);
+
+/* Diagnostics: while buf (device uint64, 8 per iteration, filled with 0xff by the caller) is
+   non-NULL, ICP launches write %globaltimer (ns) stamps of iteration it at buf[8*it + k]:
+   k = 0 selection kernel start, 1 search kernel start, 2 accumulation (or projective) kernel
+   start (each the earliest CTA), 3 the last CTA starts the final reduction, 4 solve/update
+   done.  cil_icp_iterate / cil_proj_iterate use it = 0.  NULL switches it off.  Host-only,
+   process-wide. */
+cil_status cil_debug_timestamps(uint64_t* buf);
 
 #ifdef __cplusplus
 }

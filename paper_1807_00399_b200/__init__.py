@@ -45,7 +45,8 @@ METRICS = {"point_to_point": CIL_POINT_TO_POINT, "point_to_plane": CIL_POINT_TO_
 EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_nn_query", "cil_estimate_normals",
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
             "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
-            "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin"]
+            "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin",
+            "cil_proj_workspace_bytes", "cil_proj_iterate", "cil_proj_run", "cil_debug_timestamps"]
 
 
 class cil_index_params(C.Structure):
@@ -74,6 +75,18 @@ class cil_profile_stats(C.Structure):
                 ("sel_ms", C.c_double), ("n_sel", C.c_int64)]
 
 
+class cil_intrinsics(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double)]
+
+
+def make_intrinsics(width: int, height: int, fx: float, fy: float, cx: float, cy: float) -> cil_intrinsics:
+    k = cil_intrinsics()
+    k.width, k.height = int(width), int(height)
+    k.fx, k.fy, k.cx, k.cy = float(fx), float(fy), float(cx), float(cy)
+    return k
+
+
 class cil_target_info(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_leaves", C.c_int64), ("n_nodes", C.c_int64), ("leaf_size", C.c_int32),
                 ("has_normals", C.c_int32), ("device_bytes", C.c_int64)]
@@ -96,6 +109,14 @@ _lib.cil_icp_iterate.restype = C.c_int
 _lib.cil_icp_iterate.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp, _vp, _vp]
 _lib.cil_icp_run.restype = C.c_int
 _lib.cil_icp_run.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp]
+_lib.cil_proj_workspace_bytes.restype = _sz
+_lib.cil_proj_workspace_bytes.argtypes = [_i64, C.POINTER(cil_icp_params)]
+_lib.cil_proj_iterate.restype = C.c_int
+_lib.cil_proj_iterate.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp,
+                                  _sz, _vp, _vp, _vp, _vp, _vp]
+_lib.cil_proj_run.restype = C.c_int
+_lib.cil_proj_run.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz,
+                              _vp, _vp, _vp]
 _lib.cil_status_string.restype = C.c_char_p
 _lib.cil_status_string.argtypes = [C.c_int]
 _lib.cil_last_error.restype = C.c_char_p
@@ -111,6 +132,8 @@ _lib.cil_debug_set_flags.restype = C.c_int
 _lib.cil_debug_set_flags.argtypes = [C.c_uint32]
 _lib.cil_debug_engine_trace.restype = C.c_int
 _lib.cil_debug_engine_trace.argtypes = [C.c_void_p]
+_lib.cil_debug_timestamps.restype = C.c_int
+_lib.cil_debug_timestamps.argtypes = [C.c_void_p]
 _lib.cil_debug_set_cert_skin.restype = C.c_int
 _lib.cil_debug_set_cert_skin.argtypes = [C.c_double, C.c_double, C.c_double]
 
@@ -137,6 +160,12 @@ def run_point_certified(ws: torch.Tensor) -> int:
 def run_searched(ws: torch.Tensor) -> int:
     """number of full searches cil_icp_run did (sum over iterations), read from the workspace"""
     return int(ws[WS_STATE_SEARCHED:WS_STATE_SEARCHED + 8].cpu().view(torch.int64).item())
+
+
+def debug_timestamps(buf: torch.Tensor | None) -> None:
+    """per-iteration %globaltimer stamps of the ICP kernels into buf (int64 [iters, 8], filled
+    with -1 by the caller); None switches them off (diagnostics)"""
+    _check(_lib.cil_debug_timestamps(None if buf is None else buf.data_ptr()), "cil_debug_timestamps")
 
 
 def profile_enable(on: bool = True) -> None:
@@ -333,6 +362,65 @@ def cil_icp_run(t: Target, src: torch.Tensor, pose_init: torch.Tensor, params: c
         iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev)
     _check(_lib.cil_icp_run(t.handle, _ptr(src), m, _ptr(pose_init), C.byref(params), _ptr(ws), ws.numel(),
                             _ptr(res), _ptr(iter_log), _stream_ptr(stream)), "cil_icp_run")
+    return res, iter_log
+
+
+# ---------------------------------------------------------------- projective engine (NEXT-2)
+def _organised(tgt: torch.Tensor, K: cil_intrinsics, name: str) -> None:
+    _pts(tgt, name)
+    if tgt.shape[0] != K.width * K.height:
+        raise ValueError(f"{name} must hold width*height = {K.width * K.height} points, got {tgt.shape[0]}")
+
+
+def cil_proj_workspace_bytes(m: int, params: cil_icp_params) -> int:
+    return int(_lib.cil_proj_workspace_bytes(int(m), C.byref(params)))
+
+
+def cil_proj_iterate(tgt: torch.Tensor, tgt_normals: torch.Tensor | None, K: cil_intrinsics, src: torch.Tensor,
+                     pose_in: torch.Tensor, params: cil_icp_params, ws: torch.Tensor | None = None,
+                     pose_out: torch.Tensor | None = None, want_sys: bool = True, want_corr: bool = False,
+                     stream=None):
+    """One projective-association ICP iteration on an organised target (tgt [w*h, 3] row-major
+    pixels).  Returns (pose_out, sys_bytes or None, corr_idx or None, corr_sqdist or None)."""
+    _organised(tgt, K, "tgt")
+    if tgt_normals is not None:
+        _organised(tgt_normals, K, "tgt_normals")
+    _pts(src, "src")
+    m = src.shape[0]
+    dev = src.device
+    if ws is None:
+        ws = torch.empty(cil_proj_workspace_bytes(m, params), dtype=torch.uint8, device=dev)
+    if pose_out is None:
+        pose_out = torch.empty((4, 4), dtype=torch.float64, device=dev)
+    sys_t = _struct_tensor(cil_icp_system, dev) if want_sys else None
+    ci = torch.empty(m, dtype=torch.int32, device=dev) if want_corr else None
+    cd = torch.empty(m, dtype=torch.float32, device=dev) if want_corr else None
+    _check(_lib.cil_proj_iterate(_ptr(tgt), _ptr(tgt_normals), C.byref(K), _ptr(src), m, _ptr(pose_in),
+                                 C.byref(params), _ptr(ws), ws.numel(), _ptr(pose_out), _ptr(sys_t), _ptr(ci),
+                                 _ptr(cd), _stream_ptr(stream)), "cil_proj_iterate")
+    return pose_out, sys_t, ci, cd
+
+
+def cil_proj_run(tgt: torch.Tensor, tgt_normals: torch.Tensor | None, K: cil_intrinsics, src: torch.Tensor,
+                 pose_init: torch.Tensor, params: cil_icp_params, ws: torch.Tensor | None = None,
+                 res: torch.Tensor | None = None, iter_log: torch.Tensor | None = None, want_log: bool = True,
+                 stream=None):
+    """The device-resident projective ICP loop.  Returns (res_bytes, iter_log or None)."""
+    _organised(tgt, K, "tgt")
+    if tgt_normals is not None:
+        _organised(tgt_normals, K, "tgt_normals")
+    _pts(src, "src")
+    m = src.shape[0]
+    dev = src.device
+    if ws is None:
+        ws = torch.empty(cil_proj_workspace_bytes(m, params), dtype=torch.uint8, device=dev)
+    if res is None:
+        res = _struct_tensor(cil_icp_result, dev)
+    if iter_log is None and want_log:
+        iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev)
+    _check(_lib.cil_proj_run(_ptr(tgt), _ptr(tgt_normals), C.byref(K), _ptr(src), m, _ptr(pose_init),
+                             C.byref(params), _ptr(ws), ws.numel(), _ptr(res), _ptr(iter_log), _stream_ptr(stream)),
+           "cil_proj_run")
     return res, iter_log
 
 

@@ -32,6 +32,11 @@ void cert_skin_params(double* gmin, double* gmax, double* kappa) {
     *kappa = g_skin_kappa;
 }
 void set_debug_trace(int* p) { g_trace = p; }
+namespace {
+unsigned long long* g_stamps = nullptr;
+}
+unsigned long long* debug_stamps() { return g_stamps; }
+void set_debug_stamps(unsigned long long* p) { g_stamps = p; }
 
 namespace {
 struct ProfRec { int cls; cudaEvent_t a, b; };

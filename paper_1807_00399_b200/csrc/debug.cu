@@ -9,3 +9,9 @@ CIL_API cil_status cil_debug_engine_trace(int32_t* buf) {
     cil::set_debug_trace(buf);
     return CIL_OK;
 }
+
+// Diagnostics: per-iteration %globaltimer stamps of the ICP kernels (see include/cil.h).
+CIL_API cil_status cil_debug_timestamps(uint64_t* buf) {
+    cil::set_debug_stamps(reinterpret_cast<unsigned long long*>(buf));
+    return CIL_OK;
+}

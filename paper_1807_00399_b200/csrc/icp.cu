@@ -50,7 +50,7 @@ struct IterArgs {
     float stale2;            // (max_corr_dist / 10)^2: a warm hint beyond it is stale
     const double* pose_in;
     double* pose_out;
-    double* partials;        // [kMaxCtas * kSlots]
+    double* partials;        // [kSlots][kMaxCtas] slot-major: per-CTA fp64 partial sums
     IcpState* st;
     cil_icp_system* sys;     // iterate only, nullable
     int32_t* corr_idx;       // iterate only, nullable (indexed by the caller's source order)
@@ -68,11 +68,35 @@ struct IterArgs {
     double* apose;           // [kAnchorSlots][12] pose of each anchor slot (run)
     float* adelta;           // [kAnchorSlots][16] (R - R_a | t - t_a | max|dR| | max|dt|) for the current pose
     double* iter_log;        // run only, nullable
+    // projective data association (cil_proj_*): organised target, intrinsics (R23-R25)
+    const float* ptgt;       // [pw * ph * 3] row-major pixels, caller's buffer
+    const float* pnrm;       // [pw * ph * 3] or nullptr
+    int pw, ph;
+    double pfx, pfy, pcx, pcy;
+    unsigned long long* stamps;   // diagnostics (cil_debug_timestamps), normally nullptr
     int run;
     int cert;                // run: certified warm start on
     int point_cert;          // run: the point-level certificate on (diagnostics switch)
     double rot_tol, trans_tol;
 };
+
+// Programmatic dependent launch: the per-iteration kernels are launched with the
+// programmatic-stream-serialization attribute (launch_pdl); each calls pdl_trigger() first
+// (its dependent may be scheduled once every CTA of it has started) and pdl_wait() before it
+// reads anything an earlier kernel wrote (the wait returns when the previous grid has
+// completed and flushed), so the launch latency of kernel k+1 overlaps the tail of kernel k.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// diagnostics: %globaltimer stamp k of the running iteration (first = earliest CTA)
+__device__ __forceinline__ void stamp(const IterArgs& a, int k, bool first) {
+    if (!a.stamps || threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int it = a.run ? *(volatile int*)&a.st->iters : 0;
+    if (first) atomicMin(a.stamps + 8 * it + k, t);
+    else a.stamps[8 * it + k] = t;
+}
 
 __device__ __forceinline__ float warp_transpose_reduce(float (&v)[kSlots]) {
     const int lane = threadIdx.x & 31;
@@ -90,12 +114,29 @@ __device__ __forceinline__ float warp_transpose_reduce(float (&v)[kSlots]) {
 }
 
 // ---------------------------------------------------------------- a6 + a7 (one thread)
+// The tail below runs once per iteration on one thread of one CTA (from a cold instruction
+// cache; measured with cil_debug_timestamps: ~5 us of the iteration).
+__device__ __noinline__ void rodrigues_sc(double th, double th2, double* A, double* Bc) {
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    *A = sn / th;
+    *Bc = (1.0 - cs) / th2;
+}
+
 __device__ __noinline__ void rodrigues(const double a[3], double R[9]) {
     const double th2 = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
-    const double th = sqrt(th2);
     double A, Bc;
-    if (th < 1e-4) { A = 1.0 - th2 / 6.0; Bc = 0.5 - th2 / 24.0; }
-    else { double sn, cs; sincos(th, &sn, &cs); A = sn / th; Bc = (1.0 - cs) / th2; }
+    if (th2 < 1e-4) {
+        // theta < 1e-2: sin(t)/t and (1 - cos t)/t^2 by their Taylor series through t^10
+        // (the first omitted term is < 1e-24 relative)
+        const double u = th2;
+        A = 1.0 - u * (1.0 / 6.0) * (1.0 - u * (1.0 / 20.0) * (1.0 - u * (1.0 / 42.0) * (1.0 - u * (1.0 / 72.0) *
+                                                                                      (1.0 - u * (1.0 / 110.0)))));
+        Bc = 0.5 * (1.0 - u * (1.0 / 12.0) * (1.0 - u * (1.0 / 30.0) * (1.0 - u * (1.0 / 56.0) *
+                                                                        (1.0 - u * (1.0 / 90.0) * (1.0 - u * (1.0 / 132.0))))));
+    } else {
+        rodrigues_sc(sqrt(th2), th2, &A, &Bc);
+    }
     // R = I + A [a]x + Bc [a]x^2,  [a]x^2 = a a^T - th2 I
     R[0] = 1.0 + Bc * (a[0] * a[0] - th2);
     R[4] = 1.0 + Bc * (a[1] * a[1] - th2);
@@ -182,6 +223,11 @@ __device__ __noinline__ void finalize(const IterArgs& a, const double* S, const 
     double H[36], g[6], x[6], sse, cnt;
     assemble<METRIC>(S, H, g, sse, cnt);
     const int status = solve6(H, g, cnt, x);
+    if (a.stamps) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[8 * (a.run ? a.st->iters : 0) + 6] = t;
+    }
     double Pn[16];
     for (int i = 0; i < 16; ++i) Pn[i] = P[i];
     if (status == CIL_OK) {
@@ -452,7 +498,10 @@ icp_select_kernel(const IterArgs a) {
     __shared__ double s_pose[12];
     __shared__ int s_cnt, s_np, s_base;
     __shared__ int s_pk[kSelTile / 32];
+    pdl_trigger();
+    pdl_wait();
     if (*(volatile int*)&a.st->done) return;
+    stamp(a, 0, true);
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t kslot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
@@ -600,7 +649,10 @@ struct IcpQueries {
 template <int B, bool CERT>
 __global__ void __launch_bounds__(kNNThreads, 4)
 icp_nn_kernel(const IterArgs a) {
+    pdl_trigger();
+    pdl_wait();
     if (a.run && *(volatile int*)&a.st->done) return;
+    stamp(a, 1, true);
     IcpQueries<B, CERT> qs;
     qs.src = a.src;
     qs.opts = a.T.opts;
@@ -636,14 +688,16 @@ icp_nn_kernel(const IterArgs a) {
 
 // a1 + a3 + a4 + a5 for the pair (p, t): transform, inclusive rejection (R2), residual,
 // Jacobian, fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
+// (accumulate_s: the same for an already transformed s; returns whether the pair was accepted
+// and its d^2 in *d2)
 template <int METRIC>
-__device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose34& P, float px, float py, float pz,
-                                                float4 t, float4 n, float bound2, float wpp, float wpl) {
-    const DF3 s = transform_df(P, px, py, pz);
+__device__ __forceinline__ bool accumulate_s(float (&acc)[kSlots], const DF3& s, float4 t, float4 n, float bound2,
+                                             float wpp, float wpl, float* d2) {
     const float dx = dfdiff(s.hx, s.lx, t.x);
     const float dy = dfdiff(s.hy, s.ly, t.y);
     const float dz = dfdiff(s.hz, s.lz, t.z);
-    if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= bound2)) return;
+    *d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (!(*d2 <= bound2)) return false;
     if (METRIC == CIL_COMBINED) {
         // w_pl J_pl J_pl^T + w_pp J_pp^T J_pp per pair, J_pp = [-[s]x, I3] (R22): the
         // point-to-point blocks are |s|^2 I - s s^T, [s]x, I written out per pair (no
@@ -695,17 +749,131 @@ __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose
         acc[15] += fmaf(sx, dy, -sy * dx);
         acc[16] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, acc[16])));
     }
+    return true;
+}
+
+template <int METRIC>
+__device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose34& P, float px, float py, float pz,
+                                                float4 t, float4 n, float bound2, float wpp, float wpl) {
+    float d2;
+    (void)accumulate_s<METRIC>(acc, transform_df(P, px, py, pz), t, n, bound2, wpp, wpl, &d2);
+}
+
+// ---------------------------------------------------------------- a5 reduction + a6 + a7
+// Epilogue of the accumulation kernels: warp transpose-reduce (fp32) -> per-warp fp64 ->
+// per-CTA partial; the last CTA (ticket) sums the partials in fixed order, solves, updates
+// the pose and (certified run) writes the anchor table of the next iteration.
+template <int METRIC>
+__device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[kSlots], const double* Psh) {
+    __shared__ double wsum[kIcpWarps][kSlots];
+    __shared__ double Ssum[kSlots];
+    __shared__ int last;
+    // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float mine = warp_transpose_reduce(acc);
+    wsum[warp][lane] = (double)mine;
+    __syncthreads();
+    if (threadIdx.x < kSlots) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
+        a.partials[(size_t)threadIdx.x * kMaxCtas + blockIdx.x] = v;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    stamp(a, 3, false);
+
+    // ---- last CTA: fixed-order fp64 reduction of the per-CTA partials, solve, update.
+    // Warp w sums slots w, w+8, w+16, w+24: lane l takes CTAs l, l+32, ... (coalesced rows of
+    // the slot-major partials, sixteen loads in flight), then a fixed xor-butterfly; lane 0's
+    // value is the sum (the order is a fixed function of the grid size: bitwise reproducible).
+    __threadfence();
+    {
+        const int G = (int)gridDim.x;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int b0 = 0; b0 < G; b0 += 4 * 32) {
+            double xv[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int b = b0 + 32 * u + lane;
+                    xv[q][u] = b < G ? __ldcg(a.partials + (size_t)(warp + 8 * q) * kMaxCtas + b) : 0.0;
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[q] += xv[q][u];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+            if (lane == 0) Ssum[warp + 8 * q] = v[q];
+        }
+    }
+    const int it = a.run ? a.st->iters : 0;                 // index of this iteration
+    if (a.cert && threadIdx.x < 12) a.apose[12 * (it & (kAnchorSlots - 1)) + threadIdx.x] = Psh[threadIdx.x];
+    __syncthreads();
+    const int it_stamp = a.run ? a.st->iters : 0;
+    if (a.stamps && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[8 * it_stamp + 5] = t;
+    }
+    if (threadIdx.x == 0) finalize<METRIC>(a, Ssum, Psh);
+    if (threadIdx.x == 0) {
+        if (a.stamps) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.stamps[8 * it_stamp + 4] = t;
+        }
+        a.st->ticket = 0;
+        a.st->work = 0;      // K_nn's counter, for the next iteration
+        a.st->searched += a.run ? a.st->list_n : 0;
+        a.st->list_n = 0;
+        a.st->plist_n = 0;
+    }
+    __syncthreads();
+    // anchor table for the next iteration's K_sel: delta of every live slot to the new pose
+    if (a.cert && !a.st->done) {
+        const int a_slot = threadIdx.x;
+        if (a_slot < kAnchorSlots && a_slot <= it) {
+            const double* Pa = a.apose + 12 * a_slot;
+            const volatile double* Pn = a.st->pose;
+            float* D = a.adelta + 16 * a_slot;
+            double M = 0.0, Tm = 0.0;
+            const int rot[9] = {0, 1, 2, 4, 5, 6, 8, 9, 10};
+            for (int e = 0; e < 9; ++e) {
+                const double d = Pn[rot[e]] - Pa[rot[e]];
+                D[e] = (float)d;
+                M = fmax(M, fabs(d));
+            }
+            for (int e = 0; e < 3; ++e) {
+                const double d = Pn[4 * e + 3] - Pa[4 * e + 3];
+                D[9 + e] = (float)d;
+                Tm = fmax(Tm, fabs(d));
+            }
+            D[12] = __double2float_ru(M);
+            D[13] = __double2float_ru(Tm);
+            D[14] = 0.0f;
+            D[15] = 0.0f;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
 template <int METRIC>
 __global__ void __launch_bounds__(kIcpThreads, 2)
 icp_acc_kernel(const IterArgs a) {
-    __shared__ double wsum[kIcpWarps][kSlots];
-    __shared__ double Ssum[kSlots];
     __shared__ double Psh[16];
-    __shared__ int last;
+    pdl_trigger();
+    pdl_wait();
     if (a.run && *(volatile int*)&a.st->done) return;
+    stamp(a, 2, true);
 
     if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
     __syncthreads();
@@ -748,75 +916,97 @@ icp_acc_kernel(const IterArgs a) {
             if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2, a.w_pp, a.w_pl);
     }
 
-    // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float mine = warp_transpose_reduce(acc);
-    wsum[warp][lane] = (double)mine;
-    __syncthreads();
-    if (threadIdx.x < kSlots) {
-        double v = 0.0;
-#pragma unroll
-        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
-        a.partials[(size_t)blockIdx.x * kSlots + threadIdx.x] = v;
-        __threadfence();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
+    reduce_finalize<METRIC>(a, acc, Psh);
+}
 
-    // ---- last CTA: ordered fp64 reduction of the per-CTA partials, solve, update
-    __threadfence();
-    {
-        const int k = threadIdx.x & 31, grp = threadIdx.x >> 5;
-        double v = 0.0;
-        for (int b = grp; b < (int)gridDim.x; b += kIcpWarps) v += __ldcg(a.partials + (size_t)b * kSlots + k);
-        wsum[grp][k] = v;
-    }
+// ---------------------------------------------------------------- K_proj
+// Projective data association (R23-R25): the pixel the
+// transformed source point projects to in the organised target IS its correspondence, so
+// a2 is O(1) per point and the whole iteration is one streaming kernel:
+//   a1  s = R p + t (fp64), a2' (u, v) = round(((f s) / s_z) + c) in fp64, half away from zero
+//   (CUDA round()), bounds, pixel validity (z > 0, finite), a3-a5 as K_acc on the
+//   double-float s, then the shared epilogue (fixed-order reduction, solve, pose update).
+// Source order = the caller's (an organised source projects coherently: neighbouring lanes
+// gather neighbouring pixels).
+__device__ __forceinline__ int project_pixel(const IterArgs& a, double x, double y, double z) {
+    if (!(z > 0.0)) return -1;
+    const double uf = __dadd_rn(__ddiv_rn(__dmul_rn(a.pfx, x), z), a.pcx);
+    const double vf = __dadd_rn(__ddiv_rn(__dmul_rn(a.pfy, y), z), a.pcy);
+    const double ur = round(uf), vr = round(vf);
+    if (!(ur >= 0.0 && ur < (double)a.pw && vr >= 0.0 && vr < (double)a.ph)) return -1;
+    return (int)vr * a.pw + (int)ur;
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kIcpThreads, 2)
+icp_proj_kernel(const IterArgs a) {
+    __shared__ double Psh[16];
+    pdl_trigger();
+    pdl_wait();
+    if (a.run && *(volatile int*)&a.st->done) return;
+    stamp(a, 2, true);
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
     __syncthreads();
-    if (threadIdx.x < kSlots) {
-        double v = 0.0;
+    Pose34 P;
 #pragma unroll
-        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
-        Ssum[threadIdx.x] = v;
-    }
-    const int it = a.run ? a.st->iters : 0;                 // index of this iteration
-    if (a.cert && threadIdx.x < 12) a.apose[12 * (it & (kAnchorSlots - 1)) + threadIdx.x] = Psh[threadIdx.x];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        finalize<METRIC>(a, Ssum, Psh);
-        a.st->ticket = 0;
-        a.st->work = 0;      // K_nn's counter, for the next iteration
-        a.st->searched += a.run ? a.st->list_n : 0;
-        a.st->list_n = 0;
-        a.st->plist_n = 0;
-    }
-    __syncthreads();
-    // anchor table for the next iteration's K_sel: delta of every live slot to the new pose
-    if (a.cert && !a.st->done) {
-        const int a_slot = threadIdx.x;
-        if (a_slot < kAnchorSlots && a_slot <= it) {
-            const double* Pa = a.apose + 12 * a_slot;
-            const volatile double* Pn = a.st->pose;
-            float* D = a.adelta + 16 * a_slot;
-            double M = 0.0, Tm = 0.0;
-            const int rot[9] = {0, 1, 2, 4, 5, 6, 8, 9, 10};
-            for (int e = 0; e < 9; ++e) {
-                const double d = Pn[rot[e]] - Pa[rot[e]];
-                D[e] = (float)d;
-                M = fmax(M, fabs(d));
+    for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+    float acc[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+
+    constexpr int U = 4;     // four points per trip, every load issued before the arithmetic
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += U * stride) {
+        float px[U], py[U], pz[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + u * stride;
+            px[u] = py[u] = pz[u] = 0.0f;
+            if (iu < a.m) {
+                px[u] = __ldg(a.src + 3 * (size_t)iu);
+                py[u] = __ldg(a.src + 3 * (size_t)iu + 1);
+                pz[u] = __ldg(a.src + 3 * (size_t)iu + 2);
             }
-            for (int e = 0; e < 3; ++e) {
-                const double d = Pn[4 * e + 3] - Pa[4 * e + 3];
-                D[9 + e] = (float)d;
-                Tm = fmax(Tm, fabs(d));
+        }
+        double sx[U], sy[U], sz[U];
+        int kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            sx[u] = fma(P.r[0], (double)px[u], fma(P.r[1], (double)py[u], fma(P.r[2], (double)pz[u], P.r[3])));
+            sy[u] = fma(P.r[4], (double)px[u], fma(P.r[5], (double)py[u], fma(P.r[6], (double)pz[u], P.r[7])));
+            sz[u] = fma(P.r[8], (double)px[u], fma(P.r[9], (double)py[u], fma(P.r[10], (double)pz[u], P.r[11])));
+            kk[u] = i + u * stride < a.m ? project_pixel(a, sx[u], sy[u], sz[u]) : -1;
+        }
+        float4 tt[U], nn4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            tt[u] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
+            nn4[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (kk[u] >= 0) {
+                const float* t = a.ptgt + 3 * (size_t)kk[u];
+                tt[u] = make_float4(__ldg(t), __ldg(t + 1), __ldg(t + 2), 0.0f);
+                if (METRIC != CIL_POINT_TO_POINT) {
+                    const float* n = a.pnrm + 3 * (size_t)kk[u];
+                    nn4[u] = make_float4(__ldg(n), __ldg(n + 1), __ldg(n + 2), 0.0f);
+                }
             }
-            D[12] = __double2float_ru(M);
-            D[13] = __double2float_ru(Tm);
-            D[14] = 0.0f;
-            D[15] = 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + u * stride;
+            const float4 t = tt[u];
+            const bool valid = kk[u] >= 0 && t.z > 0.0f && isfinite(t.x) && isfinite(t.y) && isfinite(t.z);
+            float d2 = INFINITY;
+            bool ok = false;
+            if (valid) ok = accumulate_s<METRIC>(acc, split_df(sx[u], sy[u], sz[u]), t, nn4[u], a.bound2, a.w_pp,
+                                                 a.w_pl, &d2);
+            if (iu < a.m) {
+                if (a.corr_idx) a.corr_idx[iu] = ok ? kk[u] : -1;
+                if (a.corr_d2) a.corr_d2[iu] = ok ? d2 : INFINITY;
+            }
         }
     }
+    reduce_finalize<METRIC>(a, acc, Psh);
 }
 
 // ---------------------------------------------------------------- run bookkeeping kernels
@@ -847,6 +1037,21 @@ __global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
 
 __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; }
 
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <class K>
 int occupancy_of(K kernel, int threads) {
     int occ = 1;
@@ -868,9 +1073,9 @@ cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
     IterArgs ad = a;
     ad.T.trace = debug_trace();
     ad.T.dbg_mode = (int)(debug_flags() >> 1) & 3;
-    icp_nn_kernel<B, CERT><<<g, kNNThreads, 0, s>>>(ad);
+    cudaError_t e = launch_pdl(icp_nn_kernel<B, CERT>, g, kNNThreads, s, ad);
     prof_end(s);
-    return cudaGetLastError();
+    return e;
 }
 
 template <bool CERT>
@@ -888,24 +1093,28 @@ cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
     static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads);
     const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
     prof_begin(kProfAcc, s);
-    icp_acc_kernel<METRIC><<<g, kIcpThreads, 0, s>>>(a);
+    cudaError_t e = launch_pdl(icp_acc_kernel<METRIC>, g, kIcpThreads, s, a);
     prof_end(s);
-    return cudaGetLastError();
+    return e;
 }
 
 // one ICP iteration = [K_sel] + K_nn + K_acc
-cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
+cudaError_t launch_iter(const IterArgs& a0, int metric, cudaStream_t s) {
+    IterArgs a = a0;
+    a.stamps = debug_stamps();
+    cudaError_t e0 = cudaSuccess;
     int n = 2;
     if (a.cert) {
         const int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
         prof_begin(kProfSel, s);
         switch (a.T.leaf_size) {
-            case 4: icp_select_kernel<4><<<g, kSelThreads, 0, s>>>(a); break;
-            case 8: icp_select_kernel<8><<<g, kSelThreads, 0, s>>>(a); break;
-            case 16: icp_select_kernel<16><<<g, kSelThreads, 0, s>>>(a); break;
-            default: icp_select_kernel<32><<<g, kSelThreads, 0, s>>>(a); break;
+            case 4: e0 = launch_pdl(icp_select_kernel<4>, g, kSelThreads, s, a); break;
+            case 8: e0 = launch_pdl(icp_select_kernel<8>, g, kSelThreads, s, a); break;
+            case 16: e0 = launch_pdl(icp_select_kernel<16>, g, kSelThreads, s, a); break;
+            default: e0 = launch_pdl(icp_select_kernel<32>, g, kSelThreads, s, a); break;
         }
         prof_end(s);
+        if (e0 != cudaSuccess) return e0;
         ++n;
     }
     count_launches(n);
@@ -915,6 +1124,27 @@ cudaError_t launch_iter(const IterArgs& a, int metric, cudaStream_t s) {
         case CIL_POINT_TO_PLANE: return launch_acc_m<CIL_POINT_TO_PLANE>(a, s);
         case CIL_COMBINED: return launch_acc_m<CIL_COMBINED>(a, s);
         default: return launch_acc_m<CIL_POINT_TO_POINT>(a, s);
+    }
+}
+
+template <int METRIC>
+cudaError_t launch_proj_m(const IterArgs& a, cudaStream_t s) {
+    static const int occ = occupancy_of(icp_proj_kernel<METRIC>, kIcpThreads);
+    const int g = persistent_grid(occ, kIcpThreads, (a.m + 3) / 4, kMaxCtas);
+    prof_begin(kProfAcc, s);
+    cudaError_t e = launch_pdl(icp_proj_kernel<METRIC>, g, kIcpThreads, s, a);
+    prof_end(s);
+    count_launches(1);
+    return e;
+}
+
+cudaError_t launch_proj(const IterArgs& a0, int metric, cudaStream_t s) {
+    IterArgs a = a0;
+    a.stamps = debug_stamps();
+    switch (metric) {
+        case CIL_POINT_TO_PLANE: return launch_proj_m<CIL_POINT_TO_PLANE>(a, s);
+        case CIL_COMBINED: return launch_proj_m<CIL_COMBINED>(a, s);
+        default: return launch_proj_m<CIL_POINT_TO_POINT>(a, s);
     }
 }
 
@@ -979,9 +1209,7 @@ cudaError_t sort_source(IterArgs& a, const float* src, cudaStream_t s) {
     return e;
 }
 
-cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
-                        void* ws, size_t ws_bytes) {
-    // parameters first (host-only, no target needed), then the target and buffers
+cil_status check_params(const char* fn, const cil_icp_params* p) {
     if (!p) { set_error("%s: NULL params", fn); return CIL_ERR_INVALID_ARG; }
     if (p->metric != CIL_POINT_TO_POINT && p->metric != CIL_POINT_TO_PLANE && p->metric != CIL_COMBINED) {
         set_error("%s: metric %d not supported", fn, p->metric);
@@ -999,6 +1227,14 @@ cil_status check_common(const char* fn, const cil_target* t, const float* src, i
     }
     if (!(p->max_corr_dist > 0.0)) { set_error("%s: max_corr_dist must be > 0", fn); return CIL_ERR_INVALID_ARG; }
     if (!(p->rot_tol >= 0.0) || !(p->trans_tol >= 0.0)) { set_error("%s: tolerances must be >= 0", fn); return CIL_ERR_INVALID_ARG; }
+    return CIL_OK;
+}
+
+cil_status check_common(const char* fn, const cil_target* t, const float* src, int64_t m, const cil_icp_params* p,
+                        void* ws, size_t ws_bytes) {
+    // parameters first (host-only, no target needed), then the target and buffers
+    cil_status rc = check_params(fn, p);
+    if (rc != CIL_OK) return rc;
     if (!t) { set_error("%s: NULL target", fn); return CIL_ERR_INVALID_ARG; }
     if (m < 0 || m > INT32_MAX) { set_error("%s: m=%lld out of range", fn, (long long)m); return CIL_ERR_INVALID_ARG; }
     if (m > 0 && !src) { set_error("%s: src is NULL", fn); return CIL_ERR_INVALID_ARG; }
@@ -1012,6 +1248,54 @@ cil_status check_common(const char* fn, const cil_target* t, const float* src, i
         return CIL_ERR_WORKSPACE;
     }
     return CIL_OK;
+}
+
+size_t proj_ws_bytes() { return 256 + align_up((size_t)kMaxCtas * kSlots * sizeof(double), 256); }
+
+cil_status check_proj(const char* fn, const float* tgt, const float* nrm, const cil_intrinsics* K, const float* src,
+                      int64_t m, const cil_icp_params* p, void* ws, size_t ws_bytes) {
+    cil_status rc = check_params(fn, p);
+    if (rc != CIL_OK) return rc;
+    if (!K) { set_error("%s: NULL intrinsics", fn); return CIL_ERR_INVALID_ARG; }
+    if (K->width < 1 || K->height < 1 || (int64_t)K->width * K->height > INT32_MAX) {
+        set_error("%s: image %d x %d out of range", fn, K->width, K->height);
+        return CIL_ERR_INVALID_ARG;
+    }
+    if (!(K->fx > 0.0) || !(K->fy > 0.0) || !std::isfinite(K->fx) || !std::isfinite(K->fy) || !std::isfinite(K->cx) ||
+        !std::isfinite(K->cy)) {
+        set_error("%s: intrinsics need finite fx, fy > 0 and finite cx, cy", fn);
+        return CIL_ERR_INVALID_ARG;
+    }
+    if (!tgt) { set_error("%s: NULL target", fn); return CIL_ERR_INVALID_ARG; }
+    if (m < 0 || m > INT32_MAX) { set_error("%s: m=%lld out of range", fn, (long long)m); return CIL_ERR_INVALID_ARG; }
+    if (m > 0 && !src) { set_error("%s: src is NULL", fn); return CIL_ERR_INVALID_ARG; }
+    if ((p->metric == CIL_POINT_TO_PLANE || p->metric == CIL_COMBINED) && !nrm) {
+        set_error("%s: point-to-plane / combined need target normals", fn);
+        return CIL_ERR_NO_NORMALS;
+    }
+    if (!ws || ((uintptr_t)ws & 255u)) { set_error("%s: workspace NULL or not 256-B aligned", fn); return CIL_ERR_WORKSPACE; }
+    if (ws_bytes < proj_ws_bytes()) {
+        set_error("%s: workspace %zu B < required %zu B", fn, ws_bytes, proj_ws_bytes());
+        return CIL_ERR_WORKSPACE;
+    }
+    return CIL_OK;
+}
+
+void bind_proj(IterArgs& a, const float* tgt, const float* nrm, const cil_intrinsics* K, const float* src, int64_t m,
+               const cil_icp_params* p, void* ws) {
+    a.st = (IcpState*)ws;
+    a.partials = (double*)((char*)ws + 256);
+    a.ptgt = tgt;
+    a.pnrm = nrm;
+    a.pw = K->width;
+    a.ph = K->height;
+    a.pfx = K->fx; a.pfy = K->fy; a.pcx = K->cx; a.pcy = K->cy;
+    a.src = src;
+    a.m = (int)m;
+    a.w_pp = (float)p->w_point;
+    a.w_pl = (float)p->w_plane;
+    a.rot_tol = p->rot_tol;
+    a.trans_tol = p->trans_tol;
 }
 
 float bound2_of(double max_dist) {
@@ -1116,6 +1400,66 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     for (int it = 0; it < params->max_iters; ++it) {
         e = launch_iter(a, params->metric, s);
         if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
+    }
+    run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
+    count_launches(1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
+    return CIL_OK;
+}
+
+// ---------------------------------------------------------------- projective engine (NEXT-2)
+CIL_API size_t cil_proj_workspace_bytes(int64_t m, const cil_icp_params* params) {
+    (void)params;
+    if (m < 0 || m > INT32_MAX) return 0;
+    return proj_ws_bytes();
+}
+
+CIL_API cil_status cil_proj_iterate(const float* tgt, const float* tgt_normals, const cil_intrinsics* K, const float* src,
+                                    int64_t m, const double* pose_in, const cil_icp_params* params, void* ws,
+                                    size_t ws_bytes, double* pose_out, cil_icp_system* sys, int32_t* corr_idx,
+                                    float* corr_sqdist, cil_stream_t stream) {
+    cil_status rc = check_proj("cil_proj_iterate", tgt, tgt_normals, K, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_in || !pose_out) { set_error("cil_proj_iterate: pose_in/pose_out NULL"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a{};
+    bind_proj(a, tgt, tgt_normals, K, src, m, params, ws);
+    a.bound2 = bound2_of(params->max_corr_dist);
+    a.pose_in = pose_in;
+    a.pose_out = pose_out;
+    a.sys = sys;
+    a.corr_idx = corr_idx;
+    a.corr_d2 = corr_sqdist;
+    cudaStream_t s = (cudaStream_t)stream;
+    reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
+    count_launches(1);
+    cudaError_t e = launch_proj(a, params->metric, s);
+    if (e != cudaSuccess) return cuda_fail(e, "icp_proj_kernel launch");
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_proj_run(const float* tgt, const float* tgt_normals, const cil_intrinsics* K, const float* src,
+                                int64_t m, const double* pose_init, const cil_icp_params* params, void* ws,
+                                size_t ws_bytes, cil_icp_result* res, double* iter_log, cil_stream_t stream) {
+    cil_status rc = check_proj("cil_proj_run", tgt, tgt_normals, K, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_init || !res) { set_error("cil_proj_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
+    if (params->max_iters < 1) { set_error("cil_proj_run: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a{};
+    bind_proj(a, tgt, tgt_normals, K, src, m, params, ws);
+    a.bound2 = bound2_of(params->max_corr_dist);
+    a.pose_in = a.st->pose;
+    a.pose_out = a.st->pose;
+    a.iter_log = iter_log;
+    a.run = 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    run_init_kernel<<<1, 256, 0, s>>>(a.st, pose_init, nullptr, nullptr, nullptr, 0, iter_log, 2 * params->max_iters);
+    count_launches(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
+    for (int it = 0; it < params->max_iters; ++it) {
+        e = launch_proj(a, params->metric, s);
+        if (e != cudaSuccess) return cuda_fail(e, "icp_proj_kernel launch");
     }
     run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
     count_launches(1);

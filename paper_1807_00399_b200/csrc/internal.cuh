@@ -84,6 +84,8 @@ unsigned debug_flags();       // cil_debug_set_flags (bit 0: no certified warm s
 int* debug_trace();           // cil_debug_engine_trace buffer (nullptr = off)
 void cert_skin_params(double* gmin, double* gmax, double* kappa);   // cil_debug_set_cert_skin
 void set_debug_trace(int* p);
+unsigned long long* debug_stamps();            // cil_debug_timestamps buffer (nullptr = off)
+void set_debug_stamps(unsigned long long* p);
 
 // diagnostics: per-launch event timing (cil_profile_*)
 enum ProfClass { kProfBuild = 0, kProfNN = 1, kProfAcc = 2, kProfQuery = 3, kProfSel = 4 };

@@ -41,11 +41,11 @@ def test_struct_layouts_match_header(cil):
 #include <stddef.h>
 #include "cil.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu\n", sizeof(cil_index_params), sizeof(cil_icp_params), sizeof(cil_icp_result),
-         sizeof(cil_icp_system), sizeof(cil_target_info));
-  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(cil_icp_params, max_corr_dist), offsetof(cil_icp_result, rmse),
+  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(cil_index_params), sizeof(cil_icp_params), sizeof(cil_icp_result),
+         sizeof(cil_icp_system), sizeof(cil_target_info), sizeof(cil_intrinsics));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", offsetof(cil_icp_params, max_corr_dist), offsetof(cil_icp_result, rmse),
          offsetof(cil_icp_result, status), offsetof(cil_icp_system, sse), offsetof(cil_icp_system, status),
-         offsetof(cil_target_info, device_bytes));
+         offsetof(cil_target_info, device_bytes), offsetof(cil_intrinsics, fx), offsetof(cil_intrinsics, cy));
   return 0;
 }
 """
@@ -55,13 +55,14 @@ int main(void) {
         open(c, "w").write(probe)
         subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
         out = subprocess.check_output([exe]).decode().split()
-    sizes = [int(x) for x in out[:5]]
-    offs = [int(x) for x in out[5:]]
+    sizes = [int(x) for x in out[:6]]
+    offs = [int(x) for x in out[6:]]
     assert sizes == [C.sizeof(cil.cil_index_params), C.sizeof(cil.cil_icp_params), C.sizeof(cil.cil_icp_result),
-                     C.sizeof(cil.cil_icp_system), C.sizeof(cil.cil_target_info)]
+                     C.sizeof(cil.cil_icp_system), C.sizeof(cil.cil_target_info), C.sizeof(cil.cil_intrinsics)]
     assert offs == [cil.cil_icp_params.max_corr_dist.offset, cil.cil_icp_result.rmse.offset,
                     cil.cil_icp_result.status.offset, cil.cil_icp_system.sse.offset,
-                    cil.cil_icp_system.status.offset, cil.cil_target_info.device_bytes.offset]
+                    cil.cil_icp_system.status.offset, cil.cil_target_info.device_bytes.offset,
+                    cil.cil_intrinsics.fx.offset, cil.cil_intrinsics.cy.offset]
 
 
 def test_host_side_argument_errors(cil):
@@ -120,3 +121,29 @@ def test_combined_metric_parameter_errors(cil):
     ok = cil.make_params("combined", 5, 0.1, w_point=0.5, w_plane=1.0)
     assert L.cil_icp_run(None, None, 10, None, C.byref(ok), None, 0, None, None, None) == cil.CIL_ERR_INVALID_ARG
     assert "target" in L.cil_last_error().decode()        # parameters passed; the NULL target is next
+
+
+def test_projective_argument_errors(cil):
+    """cil_proj_* (SURVEY.md 8(f) NEXT-2): intrinsics, normals and workspace are validated on
+    the host; the workspace is O(1) in m."""
+    L = cil.lib()
+    p = cil.make_params("point_to_plane", 5, 0.05)
+    K = cil.make_intrinsics(640, 480, 525.0, 525.0, 319.5, 239.5)
+    nb = cil.cil_proj_workspace_bytes(1000, p)
+    assert nb > 0 and nb % 256 == 0 and nb == cil.cil_proj_workspace_bytes(2_000_000, p)
+    assert cil.cil_proj_workspace_bytes(-1, p) == 0
+    fake = C.c_void_p(1 << 20)
+    ws = C.c_void_p(1 << 24)
+    args = lambda K_, nrm, m=10: (fake, nrm, C.byref(K_) if K_ is not None else None, fake, m, fake, C.byref(p), ws,
+                                  nb, fake, None, None, None, None)
+    assert L.cil_proj_iterate(*args(None, fake)) == cil.CIL_ERR_INVALID_ARG
+    for bad in (cil.make_intrinsics(0, 480, 525, 525, 1, 1), cil.make_intrinsics(640, 480, 0.0, 525, 1, 1),
+                cil.make_intrinsics(640, 480, 525, float("nan"), 1, 1), cil.make_intrinsics(1 << 16, 1 << 16, 1, 1, 0, 0)):
+        assert L.cil_proj_iterate(*args(bad, fake)) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_proj_iterate(*args(K, None)) == cil.CIL_ERR_NO_NORMALS
+    assert L.cil_proj_iterate(*args(K, fake, m=-1)) == cil.CIL_ERR_INVALID_ARG
+    a = list(args(K, fake)); a[8] = nb - 256
+    assert L.cil_proj_iterate(*a) == cil.CIL_ERR_WORKSPACE
+    p0 = cil.make_params("point_to_plane", 0, 0.05)
+    assert L.cil_proj_run(fake, fake, C.byref(K), fake, 10, fake, C.byref(p0), ws, nb, fake, None, None) == \
+        cil.CIL_ERR_INVALID_ARG

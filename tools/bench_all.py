@@ -67,6 +67,30 @@ n3, _ = cil.cil_estimate_normals(t3, 10, (0.0, 0.0, 0.0))
 emit(config="C3_depth_normals", k=10, n=w3.n, ms=nms)
 run_cfg("C3_depth", w3, "point_to_plane", w3.max_iters, normals=n3, extra={"normals": "cil_estimate_normals k=10"})
 
+# projective data association on the organised C3 frame: one
+# streaming kernel per iteration; also the per-launch kernel time (no L2 flush inside a run)
+K3 = cil.make_intrinsics(gen.W, gen.H, gen.FX, gen.FY, gen.CX, gen.CY)
+tg3, src3, P3 = d(w3.target), d(w3.source), d(np.eye(4))
+for metric in ("point_to_plane", "point_to_point"):
+    prm = cil.make_params(metric, w3.max_iters, w3.max_dist)
+    wsp = torch.empty(cil.cil_proj_workspace_bytes(w3.m, prm), dtype=torch.uint8, device="cuda")
+    res = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    nrm3 = n3 if metric != "point_to_point" else None
+    ms = timed(lambda: cil.cil_proj_run(tg3, nrm3, K3, src3, P3, prm, ws=wsp, res=res[:200], want_log=False))
+    cil.profile_enable(True)
+    cil.profile_read()
+    cil.cil_proj_run(tg3, nrm3, K3, src3, P3, prm, ws=wsp, res=res[:200], want_log=False)
+    st = cil.profile_read()
+    cil.profile_enable(False)
+    r = cil.decode_result(res[:200])
+    bpp = 24 if metric == "point_to_point" else 36
+    kern_us = 1e3 * st["acc_ms"] / max(st["n_acc"], 1)
+    emit(config="C3_depth_projective", metric=metric, n_source=w3.m, n_target=w3.n, iterations=w3.max_iters,
+         run_ms=ms, ms_per_iteration=ms / w3.max_iters, pairs_per_s=w3.m * w3.max_iters / (ms / 1e3),
+         hbm_frac=bpp * w3.m / (ms / w3.max_iters * 1e-3) / 1e9 / PEAK, kernel_us=kern_us,
+         kernel_hbm_frac=bpp * w3.m / (kern_us * 1e-6) / 1e9 / PEAK, final_rmse=r.rmse, n_corr=r.n_corr,
+         status=r.status)
+
 for metric in ("point_to_plane", "point_to_point"):
     w4 = gen.c4_lidar(metric)
     run_cfg("C4_lidar", w4, metric, w4.max_iters)

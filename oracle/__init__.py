@@ -14,6 +14,8 @@ Parity status of each function:
   proj_system / proj_run .. pinned (identity self-pairing, one-pixel shift closed form,
                              half-away-from-zero rounding, bounds/invalid/rejection cases,
                              accumulation = icp_system_from_corr on the same pairs)
+  voxel_downsample ........ pinned (SPEC two-bin example, single bin, numpy/dict hash-group
+                             brute force, half-open cube containment, idempotence)
   pca_normals ............. pinned (noise-free planes, numpy eigh on explicit neighbourhoods)
 """
 from __future__ import annotations
@@ -87,6 +89,9 @@ def lib():
                                    C.c_int, C.c_double, C.c_double, C.c_double, _f64p, C.POINTER(C.c_double),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int32), _opt(_f64p), _opt(_f64p), _opt(_f64p), _opt(_f64p)]
+        L.orc_voxel_downsample.restype = C.c_int64
+        L.orc_voxel_downsample.argtypes = [_f32p, _opt(_f32p), C.c_int64, C.c_double, _f64p, _f32p, _opt(_f32p),
+                                           _opt(_i64p)]
         L.orc_pca_normals.argtypes = [C.c_void_p, _f32p, C.c_int64, C.c_int, _f64p, _f32p, _opt(_f32p)]
         _lib = L
     return _lib
@@ -315,3 +320,18 @@ def pca_normals(pts, k: int = 10, view=(0.0, 0.0, 0.0), tree: KDTree | None = No
     rc = lib().orc_pca_normals(h, p, p.shape[0], int(k), np.asarray(view, np.float64), out, curv)
     assert rc == 0
     return out, curv
+
+
+def voxel_downsample(pts, bin_size: float, origin=(0.0, 0.0, 0.0), normals=None):
+    """voxel-grid downsampling (R27-R29): returns (points [b,3] f32, normals [b,3] or
+    None, keys [b,3] int64) in ascending key order; raises on a key outside int32"""
+    p = _pts(pts)
+    nrm = None if normals is None else _pts(normals)
+    n = p.shape[0]
+    op = np.empty((max(n, 1), 3), np.float32)
+    on = np.empty((max(n, 1), 3), np.float32) if nrm is not None else None
+    ok = np.empty((max(n, 1), 3), np.int64)
+    nb = lib().orc_voxel_downsample(p, nrm, n, float(bin_size), np.asarray(origin, np.float64), op, on, ok)
+    if nb < 0:
+        raise ValueError("voxel key outside int32 or not finite")
+    return op[:nb], (on[:nb] if on is not None else None), ok[:nb]

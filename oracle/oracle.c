@@ -29,6 +29,9 @@
  *   - projective data association for organised clouds (
  *     SPEC.md:392-400): project s through the target intrinsics, round half away from
  *     zero, take that pixel's point if valid and within max_dist.
+ *   - voxel-grid downsampling: bin key
+ *     floor((p - origin) / bin) per axis, one fp64 mean per non-empty bin (normals: mean
+ *     renormalised), bins in ascending lexicographic key order.
  *   - PCA normals over k-NN (used only to build config-3 inputs, as
  *     BASELINE.json configs[2] asks for "normals from oracle PCA over 10-NN").
  *
@@ -681,4 +684,63 @@ int orc_pca_normals(const void* kd, const float* pts, int64_t n, int k, const do
         }
     }
     return 0;
+}
+
+/* ------------------------------------------------------------------ voxel-grid downsampling */
+/* "general dimension grid-based point cloud downsampling",
+   "downsampled using a voxel grid of bin size equal to 1cm"; SPEC.md:242-256
+   (grid_downsample) and DESIGN.md readings R27-R29:
+     key_a(p) = floor((p_a - origin_a) / bin)     (fp64: promote, subtract, divide, floor)
+     output: one point per non-empty bin = the fp64 mean of its points (summed in increasing
+     input index, divided by the count, cast to fp32); normals (nullable): the fp64 mean of the
+     bin's normals, divided by its norm sqrt(x*x + y*y + z*z), or 0 if that norm < 1e-12;
+     bins in ascending lexicographic (key_x, key_y, key_z) order.
+   Returns the number of bins, or -1 when a key is not finite / outside int32. */
+typedef struct { int64_t kx, ky, kz, idx; } vox_item;
+
+static int vox_cmp(const void* a, const void* b) {
+    const vox_item* x = (const vox_item*)a;
+    const vox_item* y = (const vox_item*)b;
+    if (x->kx != y->kx) return x->kx < y->kx ? -1 : 1;
+    if (x->ky != y->ky) return x->ky < y->ky ? -1 : 1;
+    if (x->kz != y->kz) return x->kz < y->kz ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx ? 1 : 0);
+}
+
+int64_t orc_voxel_downsample(const float* pts, const float* nrm, int64_t n, double bin, const double origin[3],
+                             float* out_pts, float* out_nrm, int64_t* out_keys /* nullable [3*bins] */) {
+    if (n <= 0) return 0;
+    vox_item* it = (vox_item*)malloc((size_t)n * sizeof(vox_item));
+    for (int64_t i = 0; i < n; ++i) {
+        double k[3];
+        for (int a = 0; a < 3; ++a) {
+            k[a] = floor(((double)pts[3 * i + a] - origin[a]) / bin);
+            if (!(k[a] >= -2147483648.0 && k[a] <= 2147483647.0)) { free(it); return -1; }
+        }
+        it[i].kx = (int64_t)k[0]; it[i].ky = (int64_t)k[1]; it[i].kz = (int64_t)k[2]; it[i].idx = i;
+    }
+    qsort(it, (size_t)n, sizeof(vox_item), vox_cmp);
+    int64_t nb = 0;
+    for (int64_t s = 0; s < n;) {
+        int64_t e = s;
+        while (e < n && it[e].kx == it[s].kx && it[e].ky == it[s].ky && it[e].kz == it[s].kz) ++e;
+        double c[3] = {0.0, 0.0, 0.0}, m[3] = {0.0, 0.0, 0.0};
+        for (int64_t r = s; r < e; ++r)         /* increasing input index (the sort's tie order) */
+            for (int a = 0; a < 3; ++a) {
+                c[a] += (double)pts[3 * it[r].idx + a];
+                if (nrm) m[a] += (double)nrm[3 * it[r].idx + a];
+            }
+        const double cnt = (double)(e - s);
+        for (int a = 0; a < 3; ++a) out_pts[3 * nb + a] = (float)(c[a] / cnt);
+        if (nrm) {
+            for (int a = 0; a < 3; ++a) m[a] = m[a] / cnt;
+            const double len = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]);
+            for (int a = 0; a < 3; ++a) out_nrm[3 * nb + a] = len < 1e-12 ? 0.0f : (float)(m[a] / len);
+        }
+        if (out_keys) { out_keys[3 * nb] = it[s].kx; out_keys[3 * nb + 1] = it[s].ky; out_keys[3 * nb + 2] = it[s].kz; }
+        ++nb;
+        s = e;
+    }
+    free(it);
+    return nb;
 }

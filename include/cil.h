@@ -232,6 +232,22 @@ cil_status cil_proj_run(const float* tgt, const float* tgt_normals, const cil_in
                         const float* src, int64_t m, const double* pose_init, const cil_icp_params* params,
                         void* ws, size_t ws_bytes, cil_icp_result* res, double* iter_log, cil_stream_t stream);
 
+/* ---- Voxel-grid downsampling ----
+   PAPER.md:125 ("general dimension grid-based point cloud downsampling"), PAPER.md:195 (the ICP
+   benchmark's 1 cm voxel grid); R27-R29.  Point p falls in the bin
+   k_a = floor((p_a - origin_a) / bin_size), evaluated in fp64.  One output point per non-empty
+   bin: the fp64 mean of its points (summed in increasing input index) cast to fp32; output
+   normals (nullable; need input normals): the fp64 mean of the bin's normals divided by its
+   norm, or 0 if that norm < 1e-12.  Bins in ascending lexicographic (k_x, k_y, k_z) order.
+   pts / normals: device fp32 [n*3]; origin: HOST double[3] (NULL = 0); out_pts / out_normals:
+   device fp32 [n*3] (the worst case; the first *n_out rows are written); n_out: DEVICE int64,
+   written stream-ordered (no host synchronisation) = the number of bins, or -1 when a key is
+   not finite or an axis spans 2^21 bins or more.  n == 0 writes *n_out = 0.  Scratch ~44 B
+   per point from the library's stream-ordered pool. */
+cil_status cil_voxel_downsample(const float* pts, const float* normals, int64_t n, double bin_size,
+                                const double* origin, float* out_pts, float* out_normals, int64_t* n_out,
+                                cil_stream_t stream);
+
 /* Static strings; cil_last_error is thread-local detail for the last failing call. */
 const char* cil_status_string(cil_status s);
 const char* cil_last_error(void);

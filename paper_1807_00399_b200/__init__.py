@@ -46,7 +46,8 @@ EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_n
             "cil_icp_workspace_bytes", "cil_icp_iterate", "cil_icp_run", "cil_status_string",
             "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
             "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin",
-            "cil_proj_workspace_bytes", "cil_proj_iterate", "cil_proj_run", "cil_debug_timestamps"]
+            "cil_proj_workspace_bytes", "cil_proj_iterate", "cil_proj_run", "cil_debug_timestamps",
+            "cil_voxel_downsample"]
 
 
 class cil_index_params(C.Structure):
@@ -117,6 +118,8 @@ _lib.cil_proj_iterate.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64
 _lib.cil_proj_run.restype = C.c_int
 _lib.cil_proj_run.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz,
                               _vp, _vp, _vp]
+_lib.cil_voxel_downsample.restype = C.c_int
+_lib.cil_voxel_downsample.argtypes = [_vp, _vp, _i64, C.c_double, C.POINTER(C.c_double * 3), _vp, _vp, _vp, _vp]
 _lib.cil_status_string.restype = C.c_char_p
 _lib.cil_status_string.argtypes = [C.c_int]
 _lib.cil_last_error.restype = C.c_char_p
@@ -422,6 +425,31 @@ def cil_proj_run(tgt: torch.Tensor, tgt_normals: torch.Tensor | None, K: cil_int
                              C.byref(params), _ptr(ws), ws.numel(), _ptr(res), _ptr(iter_log), _stream_ptr(stream)),
            "cil_proj_run")
     return res, iter_log
+
+
+# ---------------------------------------------------------------- voxel-grid downsampling (NEXT-4)
+def cil_voxel_downsample(pts: torch.Tensor, bin_size: float, origin=(0.0, 0.0, 0.0),
+                         normals: torch.Tensor | None = None, stream=None, sync: bool = True):
+    """Voxel-grid downsampling on the GPU.  sync=True: returns (points [b,3], normals [b,3] or
+    None) after reading the bin count; sync=False: returns the full-size buffers and the device
+    int64 count tensor without synchronising."""
+    _pts(pts, "pts")
+    n = pts.shape[0]
+    dev = pts.device
+    if normals is not None:
+        _pts(normals, "normals")
+    out = torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev)
+    out_n = torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev) if normals is not None else None
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    o = (C.c_double * 3)(*[float(v) for v in origin])
+    _check(_lib.cil_voxel_downsample(_ptr(pts), _ptr(normals), n, float(bin_size), C.byref(o), _ptr(out), _ptr(out_n),
+                                     _ptr(cnt), _stream_ptr(stream)), "cil_voxel_downsample")
+    if not sync:
+        return out, out_n, cnt
+    nb = int(cnt.item())
+    if nb < 0:
+        raise CilError(CIL_ERR_INVALID_ARG, "cil_voxel_downsample: key not finite or axis span >= 2^21 bins")
+    return out[:nb], (out_n[:nb] if out_n is not None else None)
 
 
 # ---------------------------------------------------------------- decoded views

@@ -99,6 +99,11 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // points in that order, packed xyz); n >= 1
 cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* sorted, cudaStream_t s, int* nlaunch);
 
+// target.cu: stable LSD radix sort of (u64 key, u32 value) pairs by key bits [0, bits)
+size_t radix_sort_scratch_bytes(int n);
+cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long long* k1, uint32_t* v1, int n,
+                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt);
+
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);
 int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s);

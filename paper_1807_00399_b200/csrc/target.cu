@@ -349,6 +349,34 @@ __global__ void apply_order_kernel(const float* __restrict__ p, int n, const int
 
 }  // namespace
 
+// Stable LSD radix sort of (key, value) pairs by key bits [0, bits) in passes of 8 bits,
+// ping-ponging between (k0, v0) and (k1, v1); *in_alt = true when the result ends in (k1, v1).
+// scratch: radix_sort_scratch_bytes(n) bytes of device memory.
+size_t radix_sort_scratch_bytes(int n) {
+    const int nblk = std::max(1, (n + kTile - 1) / kTile);
+    return align_up((size_t)kRadix * nblk * 4, 256) + scan_temp_bytes((int64_t)kRadix * nblk);
+}
+
+cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long long* k1, uint32_t* v1, int n,
+                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt) {
+    const int nblk = std::max(1, (n + kTile - 1) / kTile);
+    uint32_t* hist = (uint32_t*)scratch;
+    void* scan_tmp = (char*)scratch + align_up((size_t)kRadix * nblk * 4, 256);
+    int nl = 0;
+    bool alt = false;
+    for (int shift = 0; shift < bits; shift += kRadixBits) {
+        radix_hist_kernel<<<nblk, kThreads, 0, s>>>(k0, n, shift, hist, nblk);
+        nl += 2 + scan_exclusive_u32(hist, (int64_t)kRadix * nblk, scan_tmp, s);
+        radix_scatter_kernel<<<nblk, kThreads, 0, s>>>(k0, v0, k1, v1, n, shift, hist, nblk);
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+        alt = !alt;
+    }
+    if (nlaunch) *nlaunch += nl;
+    if (in_alt) *in_alt = alt;
+    return cudaGetLastError();
+}
+
 // Spatially coherent order of a point set (SURVEY.md 7 "source Morton-sorted once per run in its
 // own frame"): the top 32 bits of the 48-bit Morton key in the set's own bounding box, stable
 // LSD radix sort (4 passes of 8 bits) -> perm (sorted position -> original index) and the

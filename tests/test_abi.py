@@ -147,3 +147,18 @@ def test_projective_argument_errors(cil):
     p0 = cil.make_params("point_to_plane", 0, 0.05)
     assert L.cil_proj_run(fake, fake, C.byref(K), fake, 10, fake, C.byref(p0), ws, nb, fake, None, None) == \
         cil.CIL_ERR_INVALID_ARG
+
+
+def test_voxel_argument_errors(cil):
+    """cil_voxel_downsample: host-side validation"""
+    L = cil.lib()
+    fake = C.c_void_p(1 << 20)
+    o = (C.c_double * 3)(0.0, 0.0, 0.0)
+    assert L.cil_voxel_downsample(fake, None, -1, 0.01, C.byref(o), fake, None, fake, None) == cil.CIL_ERR_INVALID_ARG
+    for b in (0.0, -1.0, float("nan"), float("inf")):
+        assert L.cil_voxel_downsample(fake, None, 10, b, C.byref(o), fake, None, fake, None) == cil.CIL_ERR_INVALID_ARG
+    bad = (C.c_double * 3)(0.0, float("nan"), 0.0)
+    assert L.cil_voxel_downsample(fake, None, 10, 0.01, C.byref(bad), fake, None, fake, None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_voxel_downsample(fake, None, 10, 0.01, None, fake, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_voxel_downsample(None, None, 10, 0.01, None, fake, None, fake, None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_voxel_downsample(fake, None, 10, 0.01, None, fake, fake, fake, None) == cil.CIL_ERR_NO_NORMALS

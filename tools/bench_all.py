@@ -91,6 +91,16 @@ for metric in ("point_to_plane", "point_to_point"):
          kernel_hbm_frac=bpp * w3.m / (kern_us * 1e-6) / 1e9 / PEAK, final_rmse=r.rmse, n_corr=r.n_corr,
          status=r.status)
 
+# voxel-grid downsampling: the paper's 1 cm grid on C3, 5 cm on C4
+w4v = gen.c4_lidar("point_to_plane")
+for name, pts, h in (("C3_depth", w3.target, 0.01), ("C4_lidar", w4v.target, 0.05)):
+    dp = d(pts)
+    ms = timed(lambda: cil.cil_voxel_downsample(dp, h, sync=False))
+    nb = cil.cil_voxel_downsample(dp, h)[0].shape[0]
+    emit(config=f"{name}_voxel_downsample", bin=h, n=int(pts.shape[0]), bins=nb, ms=ms,
+         points_per_s=pts.shape[0] / (ms / 1e3))
+del w4v
+
 for metric in ("point_to_plane", "point_to_point"):
     w4 = gen.c4_lidar(metric)
     run_cfg("C4_lidar", w4, metric, w4.max_iters)

@@ -66,5 +66,11 @@ if len(sys.argv) > 1:
         cil.debug_timestamps(None)
     show("C4 icp_run", st, w4.max_iters)
     s = st.cpu().numpy().astype(np.float64); s = (s - s.min()) / 1e3
-    for it in (0, 5, 20, 45):
-        print(f"  C4 it {it}: sel {s[it,1]-s[it,0]:.1f} nn {s[it,2]-s[it,1]:.1f} acc {s[it,3]-s[it,2]:.1f} tail {s[it,4]-s[it,3]:.1f}")
+    tot = {"sel": 0.0, "nn": 0.0, "acc": 0.0, "tail": 0.0, "gap": 0.0}
+    for it in range(w4.max_iters):
+        r = [s[it, 1] - s[it, 0], s[it, 2] - s[it, 1], s[it, 3] - s[it, 2], s[it, 4] - s[it, 3],
+             (s[it + 1, 0] - s[it, 4]) if it + 1 < w4.max_iters else 0.0]
+        for k, v in zip(tot, r):
+            tot[k] += v
+        print(f"  C4 it {it:2d}: sel {r[0]:7.1f} nn {r[1]:7.1f} acc {r[2]:6.1f} tail {r[3]:5.1f} gap {r[4]:5.1f}")
+    print("  C4 totals (ms):", {k: round(v / 1e3, 3) for k, v in tot.items()})

@@ -11,4 +11,8 @@ for spec in "icp_nn:3:nn_it3" "icp_nn:41:nn_it41" "icp_select:41:sel_it41" "icp_
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $s -c 1 \
       -o gpurun_out/prof_$name -f python tools/ncu_cert.py 42 > gpurun_out/ncu_$name.log 2>&1
 done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:icp_proj -s 10 -c 1 \
+    -o gpurun_out/prof_proj_c3 -f python tools/ncu_proj.py > gpurun_out/ncu_proj_c3.log 2>&1
+timeout 900 python tools/bench_all.py 5 > gpurun_out/bench_all.jsonl 2> gpurun_out/bench_all.err
+python tools/probe_stamps.py c4 > gpurun_out/stamps.log 2>&1
 ls -la gpurun_out

@@ -148,16 +148,18 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    w = _workload(args.workload, rank_seed(rank))
+    w = _workload(args.workload, rank_seed(0 if args.split else rank))
     iters = args.iters or w.max_iters
     metric = w.metric
     to_dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
     tgt = to_dev(w.target)
     nrm = to_dev(w.target_normals) if w.target_normals is not None else None
-    src = to_dev(w.source)
+    lo, hi = (rank * w.m // world, (rank + 1) * w.m // world) if args.split else (0, w.m)
+    m_rank = hi - lo
+    src = to_dev(w.source[lo:hi])
     P0 = to_dev(np.eye(4))
     prm = cil.make_params(metric, iters, w.max_dist)
-    ws = cil.alloc_workspace(w.m, prm, dev)
+    ws = cil.alloc_workspace(m_rank, prm, dev)
     res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -166,9 +168,20 @@ def run_ours(args, rank, world, local_rank):
         t = cil.cil_target_build(tgt, nrm, args.leaf)
         if evs:
             evs[1].record(stream)
-        cil.cil_icp_run(t, src, P0, prm, ws=ws, res=res, want_log=False)
+        if args.split:
+            run = cil.ShardRun(t, src, P0, prm, want_log=False, ws=ws)
+            for _ in range(iters):
+                s = run.accumulate()
+                if world > 1:
+                    dist.all_reduce(s, op=dist.ReduceOp.SUM)
+                run.finish()
+            res.copy_(run.result())
+        else:
+            cil.cil_icp_run(t, src, P0, prm, ws=ws, res=res, want_log=False)
         t.free()
 
+    if world > 1 or args.split:
+        import torch.distributed as dist
     for _ in range(args.warmup):
         flush.fill_(1)
         step()
@@ -198,8 +211,11 @@ def run_ours(args, rank, world, local_rank):
     cil.profile_enable(False)
     prof = cil.profile_read()
     launches = cil.launch_count() - launches0
-    tot_max, total_pairs = reduce_over_ranks(tot_ms, float(w.m) * iters * args.steps, world, dev)
+    tot_max, total_pairs = reduce_over_ranks(tot_ms, float(m_rank) * iters * args.steps, world, dev)
     r = cil.decode_result(res)
+    # e2e: the public host-buffer API on every rank (pinned host inputs, H2D inside the timed
+    # region, result read back to the host every step)
+    e2e = _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi) if not args.no_e2e else None
     if rank != 0:
         return None
     ms_step = tot_max / args.steps
@@ -212,16 +228,14 @@ def run_ours(args, rank, world, local_rank):
     sel_ms = prof["sel_ms"] / max(prof["n_sel"], 1) if prof["n_sel"] else 0.0
     it_ms = sel_ms + nn_ms + acc_ms
     bpp = _bytes_per_pair(metric)
-    achieved = bpp * w.m / (it_ms * 1e-3) / 1e9
+    achieved = bpp * m_rank / (it_ms * 1e-3) / 1e9
     peak, peak_src = _peak_hbm()
     traffic = _traffic_from_profiles(args.workload)
 
-    # e2e: the public host-buffer API (pinned host inputs, H2D inside the timed region,
-    # result read back to the host every step)
-    e2e = _e2e(args, w, iters, cil, dev, flush) if not args.no_e2e else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if args.split else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {
             "workload": f"{w.name}: BASELINE.json configs[3] LiDAR 64x31250, {metric}, {iters} iterations, "
@@ -231,11 +245,12 @@ def run_ours(args, rank, world, local_rank):
             "build_ms": build_ms / args.steps, "icp_ms_per_iteration": it_ms,
             "icp_select_kernel_ms": sel_ms, "icp_nn_kernel_ms": nn_ms, "icp_acc_kernel_ms": acc_ms,
             "run_ms": run_ms / args.steps,
-            "full_searches_per_run": cil.run_searched(ws) / w.m,
+            "full_searches_per_run": cil.run_searched(ws) / max(m_rank, 1),
             "timed_launches": {"select": prof["n_sel"], "nn": prof["n_nn"], "acc": prof["n_acc"],
                                "build": prof["n_build"]},
             "final_status": r.status, "final_n_corr": r.n_corr, "final_rmse": r.rmse,
-            "parallelism": f"independent frame pair per rank x{world}",
+            "parallelism": (f"one frame pair split over {world} rank(s), all-reduce of 32 fp64 per iteration"
+                            if args.split else f"independent frame pair per rank x{world}"),
         },
         "roofline": {"bound": "hbm", "kernel": "icp_select_kernel+icp_nn_kernel+icp_acc_kernel (one ICP iteration, run average)",
                      "achieved": achieved, "peak": peak,
@@ -268,20 +283,25 @@ def _traffic_from_profiles(workload):
         return None
 
 
-def _e2e(args, w, iters, cil, dev, flush):
+def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
+    """the public host-buffer path on every rank: pinned host inputs copied in, target build, the
+    run (split or not), the result read back -- all inside the timed region; (max-over-ranks
+    time, summed pairs) like the device-timed value"""
     import torch
     stream = torch.cuda.current_stream()
     h_t = torch.as_tensor(w.target).pin_memory()
     h_n = torch.as_tensor(w.target_normals).pin_memory() if w.target_normals is not None else None
-    h_s = torch.as_tensor(w.source).pin_memory()
+    h_s = torch.as_tensor(np.ascontiguousarray(w.source[lo:hi])).pin_memory()
     h_res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8).pin_memory()
     d_t = torch.empty_like(h_t, device=dev)
     d_n = torch.empty_like(h_n, device=dev) if h_n is not None else None
     d_s = torch.empty_like(h_s, device=dev)
     P0 = torch.eye(4, dtype=torch.float64, device=dev)
     prm = cil.make_params(w.metric, iters, w.max_dist)
-    ws = cil.alloc_workspace(w.m, prm, dev)
+    ws = cil.alloc_workspace(hi - lo, prm, dev)
     res = torch.zeros(C_sizeof(cil.cil_icp_result), dtype=torch.uint8, device=dev)
+    if args.split and world > 1:
+        import torch.distributed as dist
 
     def step():
         d_t.copy_(h_t, non_blocking=True)
@@ -289,7 +309,16 @@ def _e2e(args, w, iters, cil, dev, flush):
             d_n.copy_(h_n, non_blocking=True)
         d_s.copy_(h_s, non_blocking=True)
         t = cil.cil_target_build(d_t, d_n, args.leaf)
-        cil.cil_icp_run(t, d_s, P0, prm, ws=ws, res=res, want_log=False)
+        if args.split:
+            run = cil.ShardRun(t, d_s, P0, prm, want_log=False, ws=ws)
+            for _ in range(iters):
+                sm = run.accumulate()
+                if world > 1:
+                    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+                run.finish()
+            res.copy_(run.result())
+        else:
+            cil.cil_icp_run(t, d_s, P0, prm, ws=ws, res=res, want_log=False)
         h_res.copy_(res, non_blocking=True)
         t.free()
 
@@ -305,8 +334,9 @@ def _e2e(args, w, iters, cil, dev, flush):
         e1.record(stream)
         e1.synchronize()
         tot += e0.elapsed_time(e1)
+    tmax, pairs = reduce_over_ranks(tot, float(hi - lo) * iters * args.steps, world, dev)
     h2d = h_t.numel() * 4 + (h_n.numel() * 4 if h_n is not None else 0) + h_s.numel() * 4
-    return {"value": w.m * iters * args.steps / (tot / 1e3), "unit": UNIT, "ms_per_step": tot / args.steps,
+    return {"value": pairs / (tmax / 1e3), "unit": UNIT, "ms_per_step": tmax / args.steps,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h_res.numel())}
 
 
@@ -376,6 +406,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--split", action="store_true",
+                    help="one frame pair split across the ranks (SURVEY.md 8(e): NCCL all-reduce of the 32 "
+                         "fp64 sums per iteration, strong scaling) instead of one frame pair per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -202,6 +202,27 @@ cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const d
 cil_status cil_estimate_normals(const cil_target* t, int32_t k, const double* view, float* normals,
                                 float* curvature, cil_stream_t stream);
 
+/* ---- One ICP problem split across ranks ----
+   The source is partitioned across GPUs (any split; each rank passes its own shard src[m] and
+   its own workspace, the target is replicated).  Per iteration every rank calls
+   cil_icp_shard_accumulate (certificates, exact 1-NN, reject, accumulate on its shard -- the
+   steps of cil_icp_run) which writes its fp64 partial sums to sums[32] (device); the CALLER
+   sums these 32 doubles across ranks (e.g. an NCCL all-reduce on the same stream), then every
+   rank calls cil_icp_shard_finish with the reduced sums: the 6x6 solve and the pose update run
+   redundantly and give bitwise identical poses on every rank (same inputs, same code).
+   cil_icp_shard_begin sorts the shard and initialises the state (pose_init, iter_log as in
+   cil_icp_run: global {n_corr, rmse} per iteration); cil_icp_shard_result copies the state to
+   a device cil_icp_result.  Workspace: cil_icp_workspace_bytes(m).  Errors as cil_icp_run;
+   m == 0 is allowed (an empty shard contributes zero sums). */
+cil_status cil_icp_shard_begin(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                               const cil_icp_params* params, void* ws, size_t ws_bytes, double* iter_log,
+                               cil_stream_t stream);
+cil_status cil_icp_shard_accumulate(const cil_target* t, const float* src, int64_t m, const cil_icp_params* params,
+                                    void* ws, size_t ws_bytes, double* sums, cil_stream_t stream);
+cil_status cil_icp_shard_finish(const cil_target* t, int64_t m, const cil_icp_params* params, void* ws,
+                                size_t ws_bytes, const double* sums, double* iter_log, cil_stream_t stream);
+cil_status cil_icp_shard_result(void* ws, cil_icp_result* res, cil_stream_t stream);
+
 /* ---- Projective data association ----
    The paper's second correspondence engine: PAPER.md:83 ("different correspondence search
    engines (e.g., kd-tree based or projective)"), PAPER.md:140 ("one for correspondences by

@@ -47,7 +47,8 @@ EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_n
             "cil_last_error", "cil_version", "cil_launch_count", "cil_profile_enable", "cil_profile_read",
             "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin",
             "cil_proj_workspace_bytes", "cil_proj_iterate", "cil_proj_run", "cil_debug_timestamps",
-            "cil_voxel_downsample"]
+            "cil_voxel_downsample", "cil_icp_shard_begin", "cil_icp_shard_accumulate", "cil_icp_shard_finish",
+            "cil_icp_shard_result"]
 
 
 class cil_index_params(C.Structure):
@@ -118,6 +119,14 @@ _lib.cil_proj_iterate.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64
 _lib.cil_proj_run.restype = C.c_int
 _lib.cil_proj_run.argtypes = [_vp, _vp, C.POINTER(cil_intrinsics), _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz,
                               _vp, _vp, _vp]
+_lib.cil_icp_shard_begin.restype = C.c_int
+_lib.cil_icp_shard_begin.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp]
+_lib.cil_icp_shard_accumulate.restype = C.c_int
+_lib.cil_icp_shard_accumulate.argtypes = [_vp, _vp, _i64, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp]
+_lib.cil_icp_shard_finish.restype = C.c_int
+_lib.cil_icp_shard_finish.argtypes = [_vp, _i64, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp]
+_lib.cil_icp_shard_result.restype = C.c_int
+_lib.cil_icp_shard_result.argtypes = [_vp, _vp, _vp]
 _lib.cil_voxel_downsample.restype = C.c_int
 _lib.cil_voxel_downsample.argtypes = [_vp, _vp, _i64, C.c_double, C.POINTER(C.c_double * 3), _vp, _vp, _vp, _vp]
 _lib.cil_status_string.restype = C.c_char_p
@@ -425,6 +434,55 @@ def cil_proj_run(tgt: torch.Tensor, tgt_normals: torch.Tensor | None, K: cil_int
                              C.byref(params), _ptr(ws), ws.numel(), _ptr(res), _ptr(iter_log), _stream_ptr(stream)),
            "cil_proj_run")
     return res, iter_log
+
+
+# ---------------------------------------------------------------- one problem across ranks
+class ShardRun:
+    """One rank's part of an ICP problem whose source is split across ranks (C ABI
+    cil_icp_shard_*).  accumulate() -> the caller all-reduces .sums -> finish()."""
+
+    def __init__(self, t: Target, src_shard: torch.Tensor, pose_init: torch.Tensor, params: cil_icp_params,
+                 want_log: bool = True, stream=None, ws: torch.Tensor | None = None):
+        _pts(src_shard, "src_shard")
+        self.t, self.src, self.params, self.stream = t, src_shard, params, stream
+        self.m = src_shard.shape[0]
+        dev = src_shard.device
+        self.ws = ws if ws is not None else alloc_workspace(self.m, params, dev)
+        self.sums = torch.zeros(32, dtype=torch.float64, device=dev)
+        self.iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev) if want_log else None
+        _check(_lib.cil_icp_shard_begin(t.handle, _ptr(src_shard), self.m, _ptr(pose_init), C.byref(params),
+                                        _ptr(self.ws), self.ws.numel(), _ptr(self.iter_log), _stream_ptr(stream)),
+               "cil_icp_shard_begin")
+
+    def accumulate(self) -> torch.Tensor:
+        _check(_lib.cil_icp_shard_accumulate(self.t.handle, _ptr(self.src), self.m, C.byref(self.params),
+                                             _ptr(self.ws), self.ws.numel(), _ptr(self.sums),
+                                             _stream_ptr(self.stream)), "cil_icp_shard_accumulate")
+        return self.sums
+
+    def finish(self, reduced: torch.Tensor | None = None) -> None:
+        r = self.sums if reduced is None else reduced
+        _check(_lib.cil_icp_shard_finish(self.t.handle, self.m, C.byref(self.params), _ptr(self.ws), self.ws.numel(),
+                                         _ptr(r), _ptr(self.iter_log), _stream_ptr(self.stream)),
+               "cil_icp_shard_finish")
+
+    def result(self) -> torch.Tensor:
+        res = _struct_tensor(cil_icp_result, self.ws.device)
+        _check(_lib.cil_icp_shard_result(_ptr(self.ws), _ptr(res), _stream_ptr(self.stream)), "cil_icp_shard_result")
+        return res
+
+
+def icp_run_distributed(t: Target, src_shard: torch.Tensor, pose_init: torch.Tensor, params: cil_icp_params,
+                        group=None, stream=None):
+    """cil_icp_run over a source split across the ranks of torch.distributed `group`: one
+    all-reduce of 32 fp64 sums per iteration (NCCL on GPUs).  Every rank gets the same pose."""
+    import torch.distributed as dist
+    run = ShardRun(t, src_shard, pose_init, params, stream=stream)
+    for _ in range(params.max_iters):
+        s = run.accumulate()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+        run.finish()
+    return run.result(), run.iter_log
 
 
 # ---------------------------------------------------------------- voxel-grid downsampling (NEXT-4)

@@ -74,6 +74,7 @@ struct IterArgs {
     int pw, ph;
     double pfx, pfy, pcx, pcy;
     unsigned long long* stamps;   // diagnostics (cil_debug_timestamps), normally nullptr
+    double* sums_out;        // shard mode (cil_icp_shard_accumulate): the rank-local reduced sums [kSlots]
     int run;
     int cert;                // run: certified warm start on
     int point_cert;          // run: the point-level certificate on (diagnostics switch)
@@ -759,6 +760,9 @@ __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose
     (void)accumulate_s<METRIC>(acc, transform_df(P, px, py, pz), t, n, bound2, wpp, wpl, &d2);
 }
 
+template <int METRIC>
+__device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum, const double* Psh);
+
 // ---------------------------------------------------------------- a5 reduction + a6 + a7
 // Epilogue of the accumulation kernels: warp transpose-reduce (fp32) -> per-warp fp64 ->
 // per-CTA partial; the last CTA (ticket) sums the partials in fixed order, solves, updates
@@ -815,6 +819,25 @@ __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[
             if (lane == 0) Ssum[warp + 8 * q] = v[q];
         }
     }
+    __syncthreads();
+    if (a.sums_out) {                                       // shard mode: the caller all-reduces
+        if (threadIdx.x < kSlots) a.sums_out[threadIdx.x] = Ssum[threadIdx.x];
+        if (threadIdx.x == 0) {
+            a.st->ticket = 0;
+            a.st->work = 0;
+            a.st->searched += a.run ? a.st->list_n : 0;
+            a.st->list_n = 0;
+            a.st->plist_n = 0;
+        }
+        return;
+    }
+    solve_tail<METRIC>(a, Ssum, Psh);
+}
+
+// a6 + a7 and the next iteration's anchor table, from the reduced sums Ssum (shared) and the
+// pose the iteration ran at (Psh); all threads of the CTA.
+template <int METRIC>
+__device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum, const double* Psh) {
     const int it = a.run ? a.st->iters : 0;                 // index of this iteration
     if (a.cert && threadIdx.x < 12) a.apose[12 * (it & (kAnchorSlots - 1)) + threadIdx.x] = Psh[threadIdx.x];
     __syncthreads();
@@ -1033,6 +1056,21 @@ __global__ void run_final_kernel(const IcpState* st, cil_icp_result* res) {
     res->converged = st->converged;
     res->status = st->status;
     res->pad = 0;
+}
+
+// shard mode: a6 + a7 from the all-reduced sums, on every rank
+template <int METRIC>
+__global__ void __launch_bounds__(kIcpThreads)
+icp_shard_finish_kernel(const IterArgs a, const double* __restrict__ sums) {
+    __shared__ double Psh[16];
+    __shared__ double Ssum[kSlots];
+    pdl_trigger();
+    pdl_wait();
+    if (*(volatile int*)&a.st->done) return;
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.st->pose[threadIdx.x];
+    if (threadIdx.x < kSlots) Ssum[threadIdx.x] = sums[threadIdx.x];
+    __syncthreads();
+    solve_tail<METRIC>(a, Ssum, Psh);
 }
 
 __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; }
@@ -1345,14 +1383,12 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     return CIL_OK;
 }
 
-CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
-                               const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
-                               double* iter_log, cil_stream_t stream) {
-    cil_status rc = check_common("cil_icp_run", t, src, m, params, ws, ws_bytes);
-    if (rc != CIL_OK) return rc;
-    if (!pose_init || !res) { set_error("cil_icp_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
-    if (params->max_iters < 1) { set_error("cil_icp_run: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
-    IterArgs a{};
+namespace cil {
+namespace {
+// IterArgs of the device-resident loop (cil_icp_run and the shard API)
+void run_args(IterArgs& a, const cil_target* t, const float* src, int64_t m, const cil_icp_params* params, void* ws,
+              double* iter_log) {
+    a = IterArgs{};
     bind_ws(a, ws, m);
     a.T = t->v;
     a.src = src;
@@ -1388,22 +1424,109 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     a.run = 1;
     a.rot_tol = params->rot_tol;
     a.trans_tol = params->trans_tol;
-    cudaStream_t s = (cudaStream_t)stream;
+}
+
+// sorted source + state initialisation of a run
+cil_status run_begin(IterArgs& a, const float* src, int64_t m, const double* pose_init, int max_iters, cudaStream_t s) {
     cudaError_t e0 = sort_source(a, src, s);
     if (e0 != cudaSuccess) return cuda_fail(e0, "source Morton order");
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
-    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, a.gp, (int)m, iter_log,
-                                                2 * params->max_iters);
+    run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, a.gp, (int)m, a.iter_log, 2 * max_iters);
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
+    return CIL_OK;
+}
+}  // namespace
+}  // namespace cil
+
+CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                               const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                               double* iter_log, cil_stream_t stream) {
+    cil_status rc = check_common("cil_icp_run", t, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_init || !res) { set_error("cil_icp_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
+    if (params->max_iters < 1) { set_error("cil_icp_run: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a;
+    run_args(a, t, src, m, params, ws, iter_log);
+    cudaStream_t s = (cudaStream_t)stream;
+    rc = run_begin(a, src, m, pose_init, params->max_iters, s);
+    if (rc != CIL_OK) return rc;
     for (int it = 0; it < params->max_iters; ++it) {
-        e = launch_iter(a, params->metric, s);
+        cudaError_t e = launch_iter(a, params->metric, s);
         if (e != cudaSuccess) return cuda_fail(e, "icp_iter_kernel launch");
     }
     run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
     count_launches(1);
-    e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
+    return CIL_OK;
+}
+
+// ---------------------------------------------------------------- one problem across ranks
+// The source is partitioned across ranks; every rank keeps its own workspace (warm-start state
+// of its shard) and the same target.  Per iteration: cil_icp_shard_accumulate (K_sel + K_nn +
+// K_acc on the shard, rank-local fp64 sums) -> the caller's all-reduce of the 32 sums ->
+// cil_icp_shard_finish (solve + update + anchor table, redundantly and identically on every
+// rank).  iter_log of cil_icp_shard_begin receives the global {n_corr, rmse} per iteration.
+CIL_API cil_status cil_icp_shard_begin(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                                       const cil_icp_params* params, void* ws, size_t ws_bytes, double* iter_log,
+                                       cil_stream_t stream) {
+    cil_status rc = check_common("cil_icp_shard_begin", t, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!pose_init) { set_error("cil_icp_shard_begin: pose_init NULL"); return CIL_ERR_INVALID_ARG; }
+    if (params->max_iters < 1) { set_error("cil_icp_shard_begin: max_iters must be >= 1"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a;
+    run_args(a, t, src, m, params, ws, iter_log);
+    return run_begin(a, src, m, pose_init, params->max_iters, (cudaStream_t)stream);
+}
+
+CIL_API cil_status cil_icp_shard_accumulate(const cil_target* t, const float* src, int64_t m,
+                                            const cil_icp_params* params, void* ws, size_t ws_bytes, double* sums,
+                                            cil_stream_t stream) {
+    cil_status rc = check_common("cil_icp_shard_accumulate", t, src, m, params, ws, ws_bytes);
+    if (rc != CIL_OK) return rc;
+    if (!sums) { set_error("cil_icp_shard_accumulate: sums NULL"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a;
+    run_args(a, t, src, m, params, ws, nullptr);
+    a.src = (debug_flags() & 16u) ? src : a.srcs;            // the order cil_icp_shard_begin chose
+    a.sums_out = sums;
+    cudaError_t e = launch_iter(a, params->metric, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "icp shard iteration launch");
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_icp_shard_finish(const cil_target* t, int64_t m, const cil_icp_params* params, void* ws,
+                                        size_t ws_bytes, const double* sums, double* iter_log, cil_stream_t stream) {
+    cil_status rc = check_params("cil_icp_shard_finish", params);
+    if (rc != CIL_OK) return rc;
+    if (!t) { set_error("cil_icp_shard_finish: NULL target"); return CIL_ERR_INVALID_ARG; }
+    if (m < 0 || m > INT32_MAX) { set_error("cil_icp_shard_finish: m out of range"); return CIL_ERR_INVALID_ARG; }
+    if (!ws || ((uintptr_t)ws & 255u) || ws_bytes < ws_layout(m).total) {
+        set_error("cil_icp_shard_finish: workspace NULL, unaligned or too small");
+        return CIL_ERR_WORKSPACE;
+    }
+    if (!sums) { set_error("cil_icp_shard_finish: sums NULL"); return CIL_ERR_INVALID_ARG; }
+    IterArgs a;
+    run_args(a, t, nullptr, m, params, ws, iter_log);
+    a.stamps = debug_stamps();
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    switch (params->metric) {
+        case CIL_POINT_TO_PLANE: e = launch_pdl(icp_shard_finish_kernel<CIL_POINT_TO_PLANE>, 1, kIcpThreads, s, a, sums); break;
+        case CIL_COMBINED: e = launch_pdl(icp_shard_finish_kernel<CIL_COMBINED>, 1, kIcpThreads, s, a, sums); break;
+        default: e = launch_pdl(icp_shard_finish_kernel<CIL_POINT_TO_POINT>, 1, kIcpThreads, s, a, sums); break;
+    }
+    count_launches(1);
+    if (e != cudaSuccess) return cuda_fail(e, "icp_shard_finish_kernel launch");
+    return CIL_OK;
+}
+
+CIL_API cil_status cil_icp_shard_result(void* ws, cil_icp_result* res, cil_stream_t stream) {
+    if (!ws || ((uintptr_t)ws & 255u) || !res) { set_error("cil_icp_shard_result: NULL / unaligned argument"); return CIL_ERR_INVALID_ARG; }
+    run_final_kernel<<<1, 32, 0, (cudaStream_t)stream>>>((const IcpState*)ws, res);
+    count_launches(1);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
     return CIL_OK;
 }

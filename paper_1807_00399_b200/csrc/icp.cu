@@ -317,6 +317,7 @@ struct SelWarp {
     uint32_t rec[32 * kSelRounds];           // queued evaluations: index | leaf-certificate flag
     float outer[32 * kSelRounds];            // their outer bounds
     int npc;                                 // point-certified queries (diagnostics)
+    int nleaf, nlist, nitems;                // evaluations by kind (diagnostics)
 };
 
 // leaf item for K_sel: best key and the point-level second best (the loser of every merge and
@@ -446,6 +447,11 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
             sel_leaf_item<B>(a.T, nq0, l0.x, &S.best[lane], &S.sec[lane]);
         }
         const int rest = nit > 1 ? nit - 1 : 0;
+        {
+            const unsigned lf = __ballot_sync(FULL, on && nit == 1 && (S.rec[c0 + lane] >> 31) != 0);
+            const unsigned ls = __ballot_sync(FULL, on) & ~lf;
+            if (lane == 0) { S.nleaf += __popc(lf); S.nlist += __popc(ls); }
+        }
         int incl = rest;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -453,6 +459,7 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
             if (lane >= o) incl += v;
         }
         const int total = __shfl_sync(FULL, incl, 31);
+        if (lane == 0) S.nitems += total;
         if (total > 0) {
             const int excl = incl - rest;
             const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
@@ -508,7 +515,10 @@ icp_select_kernel(const IterArgs a) {
     const uint32_t kslot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     if (threadIdx.x < 12) s_pose[threadIdx.x] = a.st->pose[threadIdx.x];
     if (threadIdx.x == 0) { s_cnt = 0; s_np = 0; }
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5].npc = 0;
+    if ((threadIdx.x & 31) == 0) {
+        SelWarp& S0 = s_w[threadIdx.x >> 5];
+        S0.npc = 0; S0.nleaf = 0; S0.nlist = 0; S0.nitems = 0;
+    }
     __syncthreads();
     Pose34 P;
 #pragma unroll
@@ -538,9 +548,14 @@ icp_select_kernel(const IterArgs a) {
     if (threadIdx.x == 0) {
         s_base = s_np ? atomicAdd(&a.st->plist_n, s_np) : 0;
         if (s_cnt) atomicAdd(&a.st->list_n, s_cnt);                    // diagnostics: searched points
-        int npc = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) npc += s_w[w].npc;
+        int npc = 0, nlf = 0, nls = 0, nit = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) {
+            npc += s_w[w].npc; nlf += s_w[w].nleaf; nls += s_w[w].nlist; nit += s_w[w].nitems;
+        }
         if (npc) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->pcert_n), (unsigned long long)npc);
+        if (nlf) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->rec_leaf), (unsigned long long)nlf);
+        if (nls) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->rec_list), (unsigned long long)nls);
+        if (nit) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->rec_items), (unsigned long long)nit);
     }
     __syncthreads();
     if (threadIdx.x < s_np) a.plist[s_base + threadIdx.x] = s_pk[threadIdx.x];
@@ -1040,7 +1055,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, 
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
         st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
-        st->pcert_n = 0;
+        st->pcert_n = 0; st->rec_leaf = 0; st->rec_list = 0; st->rec_items = 0;
     }
     for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; gp[i] = 0u; }
     if (iter_log)

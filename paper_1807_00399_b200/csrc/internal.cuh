@@ -62,6 +62,9 @@ struct alignas(256) IcpState {
     int plist_n;          // 172: packets in the search list of the running iteration
     long long searched;   // 176: sum over executed iterations of list_n (diagnostics)
     long long pcert_n;    // 184: sum over iterations of point-certified points (diagnostics)
+    long long rec_leaf;   // 192: K_sel evaluations of the anchor leaf only (leaf certificate)
+    long long rec_list;   // 200: K_sel evaluations of a candidate-leaf list (list certificate)
+    long long rec_items;  // 208: leaves of those lists beyond the first
 };
 
 // Certified warm start: anchor-pose ring of cil_icp_run.

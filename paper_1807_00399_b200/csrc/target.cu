@@ -421,10 +421,12 @@ cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* 
     // 4 passes: the sorted values are back in perm
     gather_xyz_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, perm, n, sorted);
     // keep the caller's order when it is at least as coherent (scan-ordered LiDAR / depth frames)
-    cudaMemsetAsync(cticket, 0, 8, s);
-    order_choice_kernel<<<kExtBlocks, kThreads, 0, s>>>(pts, sorted, n, cpart, cticket, keep);
-    apply_order_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, n, keep, perm, sorted);
-    nl += 3;
+    if (!(debug_flags() & 32u)) {                 // diagnostics bit 5: always the Morton order
+        cudaMemsetAsync(cticket, 0, 8, s);
+        order_choice_kernel<<<kExtBlocks, kThreads, 0, s>>>(pts, sorted, n, cpart, cticket, keep);
+        apply_order_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, n, keep, perm, sorted);
+        nl += 3;
+    }
     e = cudaGetLastError();
     pool_free(tmp, s);
     if (nlaunch) *nlaunch = nl;

@@ -298,6 +298,13 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 //   float skin  (CERT only: the threshold margin g of the query just loaded)
 constexpr int kFrontierCap = 256;
 constexpr int kItemCap = 256;
+#ifndef CIL_DGROUP
+#define CIL_DGROUP 4
+#endif
+#ifndef CIL_TRACE_D
+#define CIL_TRACE_D 1
+#endif
+constexpr int kDGroup = CIL_DGROUP;      // frontier leaves tested per step of phase D
 constexpr int kDirectLeaves = 1024;
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
@@ -758,24 +765,26 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
                     if (active) thr = thr_of(best);
                     if (CERT) sThr[wid][lane] = capped ? fminf(thr, rcap2) : thr;
                 };
-                // four candidate leaves per step: their box loads are in flight together
-                for (int k = 0; k < nF; k += 4) {
-                    int f[4];
-                    float lb[4];
+                // kDGroup candidate leaves per step: their box loads are in flight together
+                for (int k = 0; k < nF; k += kDGroup) {
+                    int f[kDGroup];
+                    float lb[kDGroup];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) f[u] = k + u < nF ? F[k + u] : -1;
+                    for (int u = 0; u < kDGroup; ++u) f[u] = k + u < nF ? F[k + u] : -1;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, nq, f[u]) : INFINITY;
+                    for (int u = 0; u < kDGroup; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, nq, f[u]) : INFINITY;
+                    const float lim = capped ? fminf(thr, rcap2) : thr;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const bool need = inP && f[u] >= 0 && f[u] != hint && f[u] != hint2 &&
-                                          lb[u] <= (capped ? fminf(thr, rcap2) : thr);
+                    for (int u = 0; u < kDGroup; ++u) {
+                        const bool need = inP && f[u] >= 0 && f[u] != hint && f[u] != hint2 && lb[u] <= lim;
                         const unsigned mk = __ballot_sync(FULL, need);
                         if (need) items[nI + __popc(mk & lt)] = (f[u] << 5) | lane;
                         nI += __popc(mk);
+#if CIL_TRACE_D
                         if (tracing) dbg_items += need ? 1 : 0;
+#endif
                     }
-                    if (nI > kItemCap - 128 || (k + 4 >= nF && nI > 0)) flush();
+                    if (nI > kItemCap - 32 * kDGroup || (k + kDGroup >= nF && nI > 0)) flush();
                 }
             }
         }

@@ -75,3 +75,10 @@ def test_voxel_errors_on_device(cil):
             cil.cil_voxel_downsample(dev(p), h)
     out, _ = cil.cil_voxel_downsample(torch.empty((0, 3), dtype=torch.float32, device="cuda"), 0.1)
     assert out.shape[0] == 0
+
+
+def test_voxel_c4_full_size(cil):
+    """the full 2 M-point C4 target (BASELINE.json configs[3]) at 5 cm, with normals: bit-exact"""
+    w = W.c4("point_to_plane")
+    nb = check(cil, w.target, 0.05, nrm=w.target_normals)
+    assert 100_000 < nb < w.n

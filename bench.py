@@ -311,12 +311,21 @@ def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
     if args.split and world > 1:
         import torch.distributed as dist
 
+    s_copy = torch.cuda.Stream(device=dev)
+
     def step():
+        # target + normals first on the launching stream (the build needs them), the source on a
+        # second stream so that its copy overlaps the index build
         d_t.copy_(h_t, non_blocking=True)
         if d_n is not None:
             d_n.copy_(h_n, non_blocking=True)
-        d_s.copy_(h_s, non_blocking=True)
+        s_copy.wait_stream(stream)
+        with torch.cuda.stream(s_copy):
+            d_s.copy_(h_s, non_blocking=True)
+            ev_s = torch.cuda.Event()
+            ev_s.record(s_copy)
         t = cil.cil_target_build(d_t, d_n, args.leaf)
+        stream.wait_event(ev_s)
         if args.split:
             run = cil.ShardRun(t, d_s, P0, prm, want_log=False, ws=ws)
             for _ in range(iters):

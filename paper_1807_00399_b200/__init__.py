@@ -550,11 +550,20 @@ def icp_align(target_pts, target_normals, source_pts, metric="point_to_plane", m
             return None
         ta = torch.as_tensor(a)
         return ta.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
-    tp, tn, sp = to_dev(target_pts), to_dev(target_normals), to_dev(source_pts)
-    P0 = torch.as_tensor(np.eye(4) if pose_init is None else np.asarray(pose_init, np.float64)).to(device)
-    prm = make_params(metric, max_iters, max_corr_dist, rot_tol, trans_tol)
-    tgt = cil_target_build(tp, tn, leaf_size, stream)
-    res, _ = cil_icp_run(tgt, sp, P0, prm, want_log=False, stream=stream)
-    out = decode_result(res)
-    tgt.free(stream)
+    main = torch.cuda.current_stream(device) if stream is None else stream
+    with torch.cuda.stream(main):
+        tp, tn = to_dev(target_pts), to_dev(target_normals)
+        side = torch.cuda.Stream(device=device)      # the source copy overlaps the index build
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            sp = to_dev(source_pts)
+            P0 = torch.as_tensor(np.eye(4) if pose_init is None else np.asarray(pose_init, np.float64)).to(device)
+        prm = make_params(metric, max_iters, max_corr_dist, rot_tol, trans_tol)
+        tgt = cil_target_build(tp, tn, leaf_size, main)
+        main.wait_stream(side)
+        sp.record_stream(main)
+        P0.record_stream(main)
+        res, _ = cil_icp_run(tgt, sp, P0, prm, want_log=False, stream=main)
+        out = decode_result(res)
+    tgt.free(main)
     return out

@@ -302,7 +302,7 @@ cil_status cil_debug_set_flags(uint32_t flags);   /* bits 1-2 engine debug mode,
    (sqrt(best) + g)^2 with g = clamp(kappa * (p's displacement in the last iteration),
    min_frac * max_corr_dist, max_frac * max_corr_dist), so that its match is certified (leaf /
    candidate list) while p moves less than about g / 2 (a point moving faster than
-   4 max_frac * max_corr_dist / kappa per iteration uses the minimum).  Defaults 0.001, 0.005, 16.
+   8 max_frac * max_corr_dist / kappa per iteration uses the minimum).  Defaults 0.001, 0.006, 16.
    0 <= min_frac <= max_frac <= 1, kappa >= 0.  Host-only, process-wide. */
 cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kappa);
 

@@ -36,6 +36,12 @@ namespace cil {
 namespace {
 
 constexpr int kIcpThreads = 256;
+#ifndef CIL_SKIN_CUT
+#define CIL_SKIN_CUT 8.0f
+#endif
+// a point whose kappa x last-step displacement exceeds kSkinCut x gap_max searches with the
+// minimal skin (it would not keep a certificate anyway)
+constexpr float kSkinCut = CIL_SKIN_CUT;
 constexpr int kIcpWarps = kIcpThreads / 32;
 
 struct IterArgs {
@@ -606,7 +612,7 @@ struct IcpQueries {
             float sk = gap_min;
             if (prev_delta) {
                 const float want = kappa * displacement_bound(prev_delta, px, py, pz);
-                sk = want <= 4.0f * gap_max ? fminf(fmaxf(want, gap_min), gap_max) : gap_min;
+                sk = want <= kSkinCut * gap_max ? fminf(fmaxf(want, gap_min), gap_max) : gap_min;
             }
             skin = sk;
         }

@@ -430,18 +430,24 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
         const bool on = c0 + lane < nrec;
         int i = 0, nit = 0;
         float outer = 0.0f;
-        int4 l0 = make_int4(-1, -1, -1, -1), l1 = make_int4(-1, -1, -1, -1);
+        constexpr int NQ = kListLeaves / 4;
+        int4 lv[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) lv[c] = make_int4(-1, -1, -1, -1);
         if (on) {
             const uint32_t rec = S.rec[c0 + lane];
             outer = S.outer[c0 + lane];
             i = (int)(rec & 0x7fffffffu);
             const bool leaf_ok = (rec >> 31) != 0;
             const int4* vl = reinterpret_cast<const int4*>(a.vlist + (size_t)kListLeaves * i);
-            l0 = vl[0];
-            if (!leaf_ok) l1 = vl[1];
-            nit = leaf_ok ? 1
-                          : (l0.x >= 0) + (l0.y >= 0) + (l0.z >= 0) + (l0.w >= 0) + (l1.x >= 0) + (l1.y >= 0) +
-                                (l1.z >= 0) + (l1.w >= 0);
+            lv[0] = vl[0];
+            if (!leaf_ok)
+#pragma unroll
+                for (int c = 1; c < NQ; ++c) lv[c] = vl[c];
+            nit = 0;
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) nit += (lv[c].x >= 0) + (lv[c].y >= 0) + (lv[c].z >= 0) + (lv[c].w >= 0);
+            if (leaf_ok) nit = 1;
             const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1], a.src[3 * (size_t)i + 2]);
             S.q[0][lane] = -s.hx; S.q[1][lane] = -s.hy; S.q[2][lane] = -s.hz;
             S.q[3][lane] = -s.lx; S.q[4][lane] = -s.ly; S.q[5][lane] = -s.lz;
@@ -450,7 +456,7 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
             NegQuery nq0;
             nq0.hx = make_float2(-s.hx, -s.hx); nq0.hy = make_float2(-s.hy, -s.hy); nq0.hz = make_float2(-s.hz, -s.hz);
             nq0.lx = make_float2(-s.lx, -s.lx); nq0.ly = make_float2(-s.ly, -s.ly); nq0.lz = make_float2(-s.lz, -s.lz);
-            sel_leaf_item<B>(a.T, nq0, l0.x, &S.best[lane], &S.sec[lane]);
+            sel_leaf_item<B>(a.T, nq0, lv[0].x, &S.best[lane], &S.sec[lane]);
         }
         const int rest = nit > 1 ? nit - 1 : 0;
         {
@@ -468,7 +474,11 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
         if (lane == 0) S.nitems += total;
         if (total > 0) {
             const int excl = incl - rest;
-            const int Ls[kListLeaves] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+            int Ls[kListLeaves];
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) {
+                Ls[4 * c] = lv[c].x; Ls[4 * c + 1] = lv[c].y; Ls[4 * c + 2] = lv[c].z; Ls[4 * c + 3] = lv[c].w;
+            }
 #pragma unroll
             for (int c = 1; c < kListLeaves; ++c)
                 if (c <= rest) S.items[excl + c - 1] = (Ls[c] << 5) | lane;
@@ -661,10 +671,9 @@ struct IcpQueries {
         for (int c = 1; c < kListLeaves; ++c) if (c >= n) e[c] = -1;
         // no list, or L1 missing from a full list (an entry would be lost): no list certificate
         if (cnt == 0 || (!has_L1 && cnt == kListLeaves)) GS = 0.0f;
-        const int4 l0 = make_int4(e[0], e[1], e[2], e[3]), l1 = make_int4(e[4], e[5], e[6], e[7]);
         int4* dst = reinterpret_cast<int4*>(vlist + (size_t)kListLeaves * i);
-        dst[0] = l0;
-        dst[1] = l1;
+#pragma unroll
+        for (int c = 0; c < kListLeaves / 4; ++c) dst[c] = make_int4(e[4 * c], e[4 * c + 1], e[4 * c + 2], e[4 * c + 3]);
     }
 };
 

@@ -200,7 +200,10 @@ __device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuer
 // (linearisable: every leaf minimum that is not the final one is pushed once it loses), and
 // a leaf whose minimum is within the query's current threshold joins the query's candidate-
 // leaf list (capacity kListLeaves; the minimum of a leaf that does not fit is kept in drop).
-constexpr int kListLeaves = 8;
+#ifndef CIL_LIST_LEAVES
+#define CIL_LIST_LEAVES 12
+#endif
+constexpr int kListLeaves = CIL_LIST_LEAVES;   // multiple of 4
 struct CertSlots {
     unsigned* sec;       // leaf-level 2nd best (float bits)
     int* list;           // [kListLeaves] candidate leaves

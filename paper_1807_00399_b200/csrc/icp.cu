@@ -42,6 +42,12 @@ constexpr int kIcpThreads = 256;
 // a point whose kappa x last-step displacement exceeds kSkinCut x gap_max searches with the
 // minimal skin (it would not keep a certificate anyway)
 constexpr float kSkinCut = CIL_SKIN_CUT;
+#ifndef CIL_RHO
+#define CIL_RHO 1.1           // certificate search bound rho = CIL_RHO x max_corr_dist
+#endif
+#ifndef CIL_STALE
+#define CIL_STALE 0.01        // a warm hint beyond sqrt(CIL_STALE) x max_corr_dist also tries the cold hint
+#endif
 constexpr int kIcpWarps = kIcpThreads / 32;
 
 struct IterArgs {
@@ -1430,7 +1436,7 @@ void run_args(IterArgs& a, const cil_target* t, const float* src, int64_t m, con
     a.point_cert = (debug_flags() & 8u) ? 0 : 1;
     // certificates search to rho = 1.1 max_corr_dist so that a point with
     // nothing within rho stays provably rejected while it moves less than rho - max_corr_dist
-    const double rho = std::isinf(params->max_corr_dist) ? INFINITY : 1.1 * params->max_corr_dist;
+    const double rho = std::isinf(params->max_corr_dist) ? INFINITY : CIL_RHO * params->max_corr_dist;
     a.search2 = a.cert ? bound2_of(rho) : a.bound2;
     {
         const double gn = (rho - params->max_corr_dist) * (1.0 - 1e-6);
@@ -1447,7 +1453,7 @@ void run_args(IterArgs& a, const cil_target* t, const float* src, int64_t m, con
         a.gap_max = (float)(gmax * md);
         a.kappa = (float)kap;
     }
-    a.stale2 = std::isinf(params->max_corr_dist) ? INFINITY : (float)(0.01 * params->max_corr_dist * params->max_corr_dist);
+    a.stale2 = std::isinf(params->max_corr_dist) ? INFINITY : (float)(CIL_STALE * params->max_corr_dist * params->max_corr_dist);
     a.pose_in = a.st->pose;
     a.pose_out = a.st->pose;
     a.iter_log = iter_log;

@@ -200,6 +200,9 @@ __device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuer
 // (linearisable: every leaf minimum that is not the final one is pushed once it loses), and
 // a leaf whose minimum is within the query's current threshold joins the query's candidate-
 // leaf list (capacity kListLeaves; the minimum of a leaf that does not fit is kept in drop).
+#ifndef CIL_RCAP
+#define CIL_RCAP 8.0f         // outlier cap: a lane whose radius exceeds CIL_RCAP x the packet mean
+#endif
 #ifndef CIL_LIST_LEAVES
 #define CIL_LIST_LEAVES 12
 #endif
@@ -617,7 +620,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             rsum += __shfl_xor_sync(FULL, rsum, o);
             na += __shfl_xor_sync(FULL, na, o);
         }
-        const float rcap = 3.0f * rsum / (float)max(na, 1);
+        const float rcap = CIL_RCAP * rsum / (float)max(na, 1);
         bool normal = active && r <= rcap && r < INFINITY;
         if (T.dbg_mode == 1) normal = false;
         if (T.dbg_mode == 2) normal = active && r < INFINITY;

@@ -307,7 +307,10 @@ __device__ __forceinline__ float displacement_bound(const float* __restrict__ D,
 // a full search; K_nn then runs its packets in source order with only those lanes active, so
 // an uncertified remainder stays spatially coherent (a compacted list would scatter it).
 constexpr int kSelThreads = 256;
-constexpr int kSelRounds = 4;
+#ifndef CIL_SEL_ROUNDS
+#define CIL_SEL_ROUNDS 4
+#endif
+constexpr int kSelRounds = CIL_SEL_ROUNDS;
 constexpr int kSelTile = kSelThreads * kSelRounds;     // 1024 queries per CTA
 
 // Certificates of query i at the current pose, one query per lane, the
@@ -684,7 +687,10 @@ struct IcpQueries {
 };
 
 template <int B, bool CERT>
-__global__ void __launch_bounds__(kNNThreads, 4)
+#ifndef CIL_NN_MINB
+#define CIL_NN_MINB 4
+#endif
+__global__ void __launch_bounds__(kNNThreads, CIL_NN_MINB)
 icp_nn_kernel(const IterArgs a) {
     pdl_trigger();
     pdl_wait();

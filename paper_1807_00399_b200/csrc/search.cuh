@@ -302,7 +302,13 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 //   CERT: store(int i, best, lb_out2, const int* list, int cnt, float rS2) with the candidate-
 //   leaf list (cnt leaves; every target outside them is at d2 >= rS2; cnt = 0: no list)
 //   float skin  (CERT only: the threshold margin g of the query just loaded)
-constexpr int kFrontierCap = 256;
+#ifndef CIL_FRONTIER_CAP
+#define CIL_FRONTIER_CAP 256
+#endif
+#ifndef CIL_DIRECT_LEAVES
+#define CIL_DIRECT_LEAVES 512
+#endif
+constexpr int kFrontierCap = CIL_FRONTIER_CAP;
 constexpr int kItemCap = 256;
 #ifndef CIL_DGROUP
 #define CIL_DGROUP 4
@@ -311,7 +317,7 @@ constexpr int kItemCap = 256;
 #define CIL_TRACE_D 1
 #endif
 constexpr int kDGroup = CIL_DGROUP;      // frontier leaves tested per step of phase D
-constexpr int kDirectLeaves = 1024;
+constexpr int kDirectLeaves = CIL_DIRECT_LEAVES;
 constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
 
 // Independent per-lane exact DFS (nearest-child first, a subtree is entered iff its lower

@@ -9,7 +9,7 @@ d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 metric = os.environ.get("METRIC", "point_to_plane")
 w = gen.c4_lidar(metric)
-t = cil.cil_target_build(d(w.target), d(w.target_normals))
+t = cil.cil_target_build(d(w.target), d(w.target_normals), int(os.environ.get("LEAF", "0")))
 src, P0 = d(w.source), d(np.eye(4))
 prm = cil.make_params(metric, w.max_iters, w.max_dist)
 ws = cil.alloc_workspace(w.m, prm)

@@ -231,17 +231,13 @@ __device__ __noinline__ int solve6(const double H[36], const double g[6], double
     return CIL_OK;
 }
 
+// a6 + a7 as a pure function of the reduced sums S and the pose P: the solve x, the new pose
+// Pn (= P unless the status is CIL_OK), the system (H, g), sse and the pair count
 template <int METRIC>
-__device__ __noinline__ void finalize(const IterArgs& a, const double* S, const double* P) {
-    double H[36], g[6], x[6], sse, cnt;
+__device__ __forceinline__ int solve_pose(const double* S, const double* P, double H[36], double g[6], double x[6],
+                                          double Pn[16], double& sse, double& cnt) {
     assemble<METRIC>(S, H, g, sse, cnt);
     const int status = solve6(H, g, cnt, x);
-    if (a.stamps) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.stamps[8 * (a.run ? a.st->iters : 0) + 6] = t;
-    }
-    double Pn[16];
     for (int i = 0; i < 16; ++i) Pn[i] = P[i];
     if (status == CIL_OK) {
         double dR[9];
@@ -252,6 +248,140 @@ __device__ __noinline__ void finalize(const IterArgs& a, const double* S, const 
             Pn[4 * i + 3] = dR[3 * i] * P[3] + dR[3 * i + 1] * P[7] + dR[3 * i + 2] * P[11] + x[3 + i];
         }
         Pn[12] = 0.0; Pn[13] = 0.0; Pn[14] = 0.0; Pn[15] = 1.0;
+    }
+    return status;
+}
+
+// The same solve by one whole warp, register-resident (the persistent projective loop, where
+// it runs every iteration on every SM from a warm instruction cache): lane i < 6 holds row i
+// of H and of the factor L; column j takes lane j's pivot and L's row j by shuffles, lanes
+// i > j form L[i][j] in parallel; reciprocal pivots from rsqrt (1 ulp); every lane then runs
+// both triangular solves on a shuffled copy of L.  H and g in shared memory; returns the status
+// (uniform over the warp) and x (every lane).
+__device__ __forceinline__ int solve6_warp(const double* Hs, const double* gs, double cnt, double (&x)[6]) {
+    const int lane = threadIdx.x & 31;
+    const int r = lane < 6 ? lane : 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) x[i] = 0.0;
+    if (cnt == 0.0) return CIL_NO_CORRESPONDENCES;
+    if (cnt < 6.0) return CIL_ERR_DEGENERATE;
+    double h[6], l[6], rinv[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { h[k] = Hs[6 * r + k]; l[k] = 0.0; }
+    double pmin = INFINITY, pmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        double lj[6];
+#pragma unroll
+        for (int k = 0; k < j; ++k) lj[k] = __shfl_sync(0xffffffffu, l[k], j);
+        double v = h[j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v -= l[k] * lj[k];
+        const double d = __shfl_sync(0xffffffffu, v, j);
+        if (!(d > 0.0)) return CIL_ERR_DEGENERATE;
+        pmin = fmin(pmin, d);
+        pmax = fmax(pmax, d);
+        const double iv = rsqrt(d);
+        rinv[j] = iv;
+        l[j] = lane == j ? d * iv : (lane > j ? v * iv : 0.0);
+    }
+    if (pmin < 1e-12 * pmax) return CIL_ERR_DEGENERATE;
+    double L[6][6];
+#pragma unroll
+    for (int i = 1; i < 6; ++i)
+#pragma unroll
+        for (int k = 0; k < i; ++k) L[i][k] = __shfl_sync(0xffffffffu, l[k], i);
+    double y[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        double v = -gs[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v -= L[i][k] * y[k];
+        y[i] = v * rinv[i];
+    }
+#pragma unroll
+    for (int i = 5; i >= 0; --i) {
+        double v = y[i];
+#pragma unroll
+        for (int k = i + 1; k < 6; ++k) v -= L[k][i] * x[k];
+        x[i] = v * rinv[i];
+    }
+    return CIL_OK;
+}
+
+// a6 + a7 by one warp (all 32 lanes; every lane ends with the same x and Pn): lane 0 assembles
+// H and g into shared memory, solve6_warp, then every lane composes the pose (identical
+// arithmetic on every lane).  Hs / gsh / scal: shared scratch (36 / 6 / 2 doubles).
+template <int METRIC>
+__device__ __forceinline__ int solve_pose_warp(const double* S, const double* P, double* Hs, double* gsh, double* scal,
+                                               double (&x)[6], double (&Pn)[16]) {
+    if ((threadIdx.x & 31) == 0) assemble<METRIC>(S, Hs, gsh, scal[0], scal[1]);
+    __syncwarp();
+    const int status = solve6_warp(Hs, gsh, scal[1], x);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Pn[i] = P[i];
+    if (status == CIL_OK) {
+        double dR[9];
+        rodrigues(x, dR);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                Pn[4 * i + j] = dR[3 * i] * P[j] + dR[3 * i + 1] * P[4 + j] + dR[3 * i + 2] * P[8 + j];
+            Pn[4 * i + 3] = dR[3 * i] * P[3] + dR[3 * i + 1] * P[7] + dR[3 * i + 2] * P[11] + x[3 + i];
+        }
+        Pn[12] = 0.0; Pn[13] = 0.0; Pn[14] = 0.0; Pn[15] = 1.0;
+    }
+    return status;
+}
+
+// finalize with the warp solve (warp 0 of the last CTA; the projective engine)
+template <int METRIC>
+__device__ __noinline__ void finalize_warp(const IterArgs& a, const double* S, const double* P) {
+    __shared__ double Hs[36], gsh[6], scal[2];
+    double x[6], Pn[16];
+    const int status = solve_pose_warp<METRIC>(S, P, Hs, gsh, scal, x, Pn);
+    if ((threadIdx.x & 31) != 0) return;
+    const double sse = scal[0], cnt = scal[1];
+    const double rmse = cnt > 0.0 ? sqrt(sse / cnt) : 0.0;
+    if (a.run) {
+        IcpState* st = a.st;
+        const int it = st->iters;
+        if (a.iter_log) { a.iter_log[2 * it] = cnt; a.iter_log[2 * it + 1] = rmse; }
+        st->iters = it + 1;
+        st->n_corr = (long long)cnt;
+        st->rmse = rmse;
+        if (status != CIL_OK) {
+            st->status = status;
+            st->converged = 0;
+            st->done = 1;
+        } else {
+            for (int i = 0; i < 16; ++i) st->pose[i] = Pn[i];
+            const double th = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+            const double tn = sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+            if (th < a.rot_tol && tn < a.trans_tol) { st->converged = 1; st->done = 1; }
+        }
+    } else {
+        for (int i = 0; i < 16; ++i) a.pose_out[i] = Pn[i];
+        if (a.sys) {
+            for (int i = 0; i < 36; ++i) a.sys->H[i] = Hs[i];
+            for (int i = 0; i < 6; ++i) { a.sys->g[i] = gsh[i]; a.sys->x[i] = x[i]; }
+            a.sys->sse = sse;
+            a.sys->n_corr = (long long)cnt;
+            a.sys->status = status;
+            a.sys->pad = 0;
+        }
+    }
+}
+
+template <int METRIC>
+__device__ __noinline__ void finalize(const IterArgs& a, const double* S, const double* P) {
+    double H[36], g[6], x[6], Pn[16], sse, cnt;
+    const int status = solve_pose<METRIC>(S, P, H, g, x, Pn, sse, cnt);
+    if (a.stamps) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[8 * (a.run ? a.st->iters : 0) + 6] = t;
     }
     const double rmse = cnt > 0.0 ? sqrt(sse / cnt) : 0.0;
     if (a.run) {
@@ -802,19 +932,9 @@ __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose
     (void)accumulate_s<METRIC>(acc, transform_df(P, px, py, pz), t, n, bound2, wpp, wpl, &d2);
 }
 
-template <int METRIC>
-__device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum, const double* Psh);
-
-// ---------------------------------------------------------------- a5 reduction + a6 + a7
-// Epilogue of the accumulation kernels: warp transpose-reduce (fp32) -> per-warp fp64 ->
-// per-CTA partial; the last CTA (ticket) sums the partials in fixed order, solves, updates
-// the pose and (certified run) writes the anchor table of the next iteration.
-template <int METRIC>
-__device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[kSlots], const double* Psh) {
-    __shared__ double wsum[kIcpWarps][kSlots];
-    __shared__ double Ssum[kSlots];
-    __shared__ int last;
-    // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
+// Per-CTA partial of the 32 fp32 per-thread sums: warp transpose-reduce (fp32) -> per-warp fp64
+// -> fixed-order sum over the warps -> partials[slot * kMaxCtas + blockIdx.x] (slot-major)
+__device__ __forceinline__ void cta_partial(float (&acc)[kSlots], double (*wsum)[kSlots], double* partials) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float mine = warp_transpose_reduce(acc);
     wsum[warp][lane] = (double)mine;
@@ -823,9 +943,54 @@ __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[
         double v = 0.0;
 #pragma unroll
         for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
-        a.partials[(size_t)threadIdx.x * kMaxCtas + blockIdx.x] = v;
+        partials[(size_t)threadIdx.x * kMaxCtas + blockIdx.x] = v;
         __threadfence();
     }
+}
+
+// Fixed-order fp64 sum of G slot-major per-CTA partials into Ssum (all threads of the CTA):
+// warp w sums slots w, w+8, w+16, w+24: lane l takes CTAs l, l+32, ... (coalesced rows,
+// sixteen loads in flight), then a fixed xor-butterfly; lane 0's value is the sum (the order is
+// a fixed function of G: bitwise reproducible, and identical in every CTA that runs it).
+__device__ __forceinline__ void sum_partials(const double* partials, int G, double* Ssum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b0 = 0; b0 < G; b0 += 4 * 32) {
+        double xv[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int b = b0 + 32 * u + lane;
+                xv[q][u] = b < G ? __ldcg(partials + (size_t)(warp + 8 * q) * kMaxCtas + b) : 0.0;
+            }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[q] += xv[q][u];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+        if (lane == 0) Ssum[warp + 8 * q] = v[q];
+    }
+}
+
+template <int METRIC, bool WARP = false>
+__device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum, const double* Psh);
+
+// ---------------------------------------------------------------- a5 reduction + a6 + a7
+// Epilogue of the accumulation kernels: warp transpose-reduce (fp32) -> per-warp fp64 ->
+// per-CTA partial; the last CTA (ticket) sums the partials in fixed order, solves, updates
+// the pose and (certified run) writes the anchor table of the next iteration.
+template <int METRIC, bool WARP = false>
+__device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[kSlots], const double* Psh) {
+    __shared__ double wsum[kIcpWarps][kSlots];
+    __shared__ double Ssum[kSlots];
+    __shared__ int last;
+    // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
+    cta_partial(acc, wsum, a.partials);
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
     __syncthreads();
@@ -837,30 +1002,7 @@ __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[
     // the slot-major partials, sixteen loads in flight), then a fixed xor-butterfly; lane 0's
     // value is the sum (the order is a fixed function of the grid size: bitwise reproducible).
     __threadfence();
-    {
-        const int G = (int)gridDim.x;
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int b0 = 0; b0 < G; b0 += 4 * 32) {
-            double xv[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = b0 + 32 * u + lane;
-                    xv[q][u] = b < G ? __ldcg(a.partials + (size_t)(warp + 8 * q) * kMaxCtas + b) : 0.0;
-                }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[q] += xv[q][u];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
-            if (lane == 0) Ssum[warp + 8 * q] = v[q];
-        }
-    }
+    sum_partials(a.partials, (int)gridDim.x, Ssum);
     __syncthreads();
     if (a.sums_out) {                                       // shard mode: the caller all-reduces
         if (threadIdx.x < kSlots) a.sums_out[threadIdx.x] = Ssum[threadIdx.x];
@@ -873,12 +1015,12 @@ __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[
         }
         return;
     }
-    solve_tail<METRIC>(a, Ssum, Psh);
+    solve_tail<METRIC, WARP>(a, Ssum, Psh);
 }
 
 // a6 + a7 and the next iteration's anchor table, from the reduced sums Ssum (shared) and the
 // pose the iteration ran at (Psh); all threads of the CTA.
-template <int METRIC>
+template <int METRIC, bool WARP>
 __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum, const double* Psh) {
     const int it = a.run ? a.st->iters : 0;                 // index of this iteration
     if (a.cert && threadIdx.x < 12) a.apose[12 * (it & (kAnchorSlots - 1)) + threadIdx.x] = Psh[threadIdx.x];
@@ -889,7 +1031,11 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.stamps[8 * it_stamp + 5] = t;
     }
-    if (threadIdx.x == 0) finalize<METRIC>(a, Ssum, Psh);
+    if (WARP) {
+        if (threadIdx.x < 32) finalize_warp<METRIC>(a, Ssum, Psh);
+    } else if (threadIdx.x == 0) {
+        finalize<METRIC>(a, Ssum, Psh);
+    }
     if (threadIdx.x == 0) {
         if (a.stamps) {
             unsigned long long t;
@@ -1002,23 +1148,10 @@ __device__ __forceinline__ int project_pixel(const IterArgs& a, double x, double
     return (int)vr * a.pw + (int)ur;
 }
 
+// the streaming body of the projective iteration: a1, a2', a3-a5 for this thread's points
+// (grid-stride, four per trip); corr outputs when requested (iterate)
 template <int METRIC>
-__global__ void __launch_bounds__(kIcpThreads, 2)
-icp_proj_kernel(const IterArgs a) {
-    __shared__ double Psh[16];
-    pdl_trigger();
-    pdl_wait();
-    if (a.run && *(volatile int*)&a.st->done) return;
-    stamp(a, 2, true);
-    if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
-    __syncthreads();
-    Pose34 P;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
-    float acc[kSlots];
-#pragma unroll
-    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
-
+__device__ __forceinline__ void proj_accumulate(const IterArgs& a, const Pose34& P, float (&acc)[kSlots]) {
     constexpr int U = 4;     // four points per trip, every load issued before the arithmetic
     const int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += U * stride) {
@@ -1071,7 +1204,128 @@ icp_proj_kernel(const IterArgs a) {
             }
         }
     }
-    reduce_finalize<METRIC>(a, acc, Psh);
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kIcpThreads, 2)
+icp_proj_kernel(const IterArgs a) {
+    __shared__ double Psh[16];
+    pdl_trigger();
+    pdl_wait();
+    if (a.run && *(volatile int*)&a.st->done) return;
+    stamp(a, 2, true);
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
+    __syncthreads();
+    Pose34 P;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+    float acc[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+
+    proj_accumulate<METRIC>(a, P, acc);
+    reduce_finalize<METRIC, true>(a, acc, Psh);
+}
+
+// Grid-wide barrier of a cooperatively launched grid (every CTA co-resident): arrival counter +
+// generation word in the workspace state.
+__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(const_cast<unsigned*>(gen), 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// The whole projective loop in one persistent launch (cil_proj_run): per iteration every CTA
+// streams its points, writes its partial (double-buffered by iteration parity), meets the
+// others at one grid barrier, then EVERY CTA sums all partials in the same fixed order and
+// solves redundantly -- identical inputs, identical code, so every CTA holds the bitwise same
+// new pose (and the loop equals the chain of cil_proj_iterate launches bit for bit: same grid,
+// same point assignment, same reduction order).  CTA 0 writes the run state.  No launch gap,
+// no last-CTA hand-off; the solve runs from a warm instruction cache on every SM.
+template <int METRIC>
+__global__ void __launch_bounds__(kIcpThreads, 2)
+icp_proj_run_kernel(const IterArgs a, int iters) {
+    __shared__ double Psh[16];
+    __shared__ double wsum[kIcpWarps][kSlots];
+    __shared__ double Ssum[kSlots];
+    __shared__ double Hs[36], gsh[6], scal[2];
+    __shared__ int s_stop;
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.st->pose[threadIdx.x];
+    __syncthreads();
+    auto tick = [&](int it, int k) {
+        if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.stamps[8 * it + k] = t;
+        }
+    };
+    for (int it = 0; it < iters; ++it) {
+        tick(it, 0);
+        Pose34 P;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+        float acc[kSlots];
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+        proj_accumulate<METRIC>(a, P, acc);
+        double* part = a.partials + (size_t)(it & 1) * kSlots * kMaxCtas;
+        cta_partial(acc, wsum, part);
+        tick(it, 1);
+        grid_barrier(&a.st->bar_count, &a.st->bar_gen);
+        tick(it, 2);
+        sum_partials(part, (int)gridDim.x, Ssum);
+        __syncthreads();
+        tick(it, 3);
+        if (threadIdx.x < 32) {
+            double x[6], Pn[16];
+            const int status = solve_pose_warp<METRIC>(Ssum, Psh, Hs, gsh, scal, x, Pn);
+            __syncwarp();
+            if (threadIdx.x == 0) {
+                const double sse = scal[0], cnt = scal[1];
+                bool stop = status != CIL_OK;
+                bool conv = false;
+                if (!stop) {
+                    const double th = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+                    const double tn = sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+                    conv = th < a.rot_tol && tn < a.trans_tol;
+                    stop = conv;
+                }
+                if (blockIdx.x == 0) {
+                    IcpState* st = a.st;
+                    const double rmse = cnt > 0.0 ? sqrt(sse / cnt) : 0.0;
+                    if (a.iter_log) { a.iter_log[2 * it] = cnt; a.iter_log[2 * it + 1] = rmse; }
+                    st->iters = it + 1;
+                    st->n_corr = (long long)cnt;
+                    st->rmse = rmse;
+                    if (status != CIL_OK) {
+                        st->status = status;
+                        st->converged = 0;
+                        st->done = 1;
+                    } else {
+                        for (int i = 0; i < 16; ++i) st->pose[i] = Pn[i];
+                        if (conv) { st->converged = 1; st->done = 1; }
+                    }
+                }
+                if (status == CIL_OK)
+                    for (int i = 0; i < 16; ++i) Psh[i] = Pn[i];
+                s_stop = stop;
+            }
+        }
+        __syncthreads();
+        tick(it, 4);
+        if (s_stop) break;
+    }
 }
 
 // ---------------------------------------------------------------- run bookkeeping kernels
@@ -1083,6 +1337,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, 
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
         st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
         st->pcert_n = 0; st->rec_leaf = 0; st->rec_list = 0; st->rec_items = 0;
+        st->bar_count = 0; st->bar_gen = 0;
     }
     for (int i = tid; i < m; i += gridDim.x * blockDim.x) { nn[i] = -1; gw[i] = 0u; gp[i] = 0u; }
     if (iter_log)
@@ -1218,6 +1473,32 @@ cudaError_t launch_proj_m(const IterArgs& a, cudaStream_t s) {
     return e;
 }
 
+template <int METRIC>
+cudaError_t launch_proj_run_m(const IterArgs& a, int iters, cudaStream_t s) {
+    static const int occ = occupancy_of(icp_proj_kernel<METRIC>, kIcpThreads);
+    static const int occ_run = occupancy_of(icp_proj_run_kernel<METRIC>, kIcpThreads);
+    const int g = persistent_grid(occ, kIcpThreads, (a.m + 3) / 4, kMaxCtas);    // the iterate grid
+    if (g > occ_run * sm_count()) return cudaErrorCooperativeLaunchTooLarge;
+    IterArgs ad = a;
+    ad.stamps = debug_stamps();
+    int it = iters;
+    void* args[] = {(void*)&ad, (void*)&it};
+    prof_begin(kProfAcc, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)icp_proj_run_kernel<METRIC>, dim3(g), dim3(kIcpThreads),
+                                                args, 0, s);
+    prof_end(s);
+    count_launches(1);
+    return e;
+}
+
+cudaError_t launch_proj_run(const IterArgs& a, int metric, int iters, cudaStream_t s) {
+    switch (metric) {
+        case CIL_POINT_TO_PLANE: return launch_proj_run_m<CIL_POINT_TO_PLANE>(a, iters, s);
+        case CIL_COMBINED: return launch_proj_run_m<CIL_COMBINED>(a, iters, s);
+        default: return launch_proj_run_m<CIL_POINT_TO_POINT>(a, iters, s);
+    }
+}
+
 cudaError_t launch_proj(const IterArgs& a0, int metric, cudaStream_t s) {
     IterArgs a = a0;
     a.stamps = debug_stamps();
@@ -1330,7 +1611,7 @@ cil_status check_common(const char* fn, const cil_target* t, const float* src, i
     return CIL_OK;
 }
 
-size_t proj_ws_bytes() { return 256 + align_up((size_t)kMaxCtas * kSlots * sizeof(double), 256); }
+size_t proj_ws_bytes() { return 256 + align_up(2 * (size_t)kMaxCtas * kSlots * sizeof(double), 256); }
 
 cil_status check_proj(const char* fn, const float* tgt, const float* nrm, const cil_intrinsics* K, const float* src,
                       int64_t m, const cil_icp_params* p, void* ws, size_t ws_bytes) {
@@ -1622,9 +1903,15 @@ CIL_API cil_status cil_proj_run(const float* tgt, const float* tgt_normals, cons
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "run_init_kernel launch");
-    for (int it = 0; it < params->max_iters; ++it) {
-        e = launch_proj(a, params->metric, s);
-        if (e != cudaSuccess) return cuda_fail(e, "icp_proj_kernel launch");
+    // one persistent cooperative launch for the whole loop; per-iteration launches if the device
+    // cannot co-schedule the grid (same results: same grid, same arithmetic)
+    e = launch_proj_run(a, params->metric, params->max_iters, s);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        for (int it = 0; it < params->max_iters; ++it) {
+            e = launch_proj(a, params->metric, s);
+            if (e != cudaSuccess) return cuda_fail(e, "icp_proj_kernel launch");
+        }
     }
     run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
     count_launches(1);

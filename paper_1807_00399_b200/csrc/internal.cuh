@@ -65,6 +65,8 @@ struct alignas(256) IcpState {
     long long rec_leaf;   // 192: K_sel evaluations of the anchor leaf only (leaf certificate)
     long long rec_list;   // 200: K_sel evaluations of a candidate-leaf list (list certificate)
     long long rec_items;  // 208: leaves of those lists beyond the first
+    unsigned int bar_count;  // 216: grid barrier of the persistent projective loop
+    unsigned int bar_gen;    // 220
 };
 
 // Certified warm start: anchor-pose ring of cil_icp_run.

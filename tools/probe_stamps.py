@@ -1,7 +1,7 @@
 """Per-iteration timeline of the ICP kernels from %globaltimer stamps (cil_debug_timestamps):
 gaps between kernels, body and the last-CTA tail (reduction + solve), in microseconds."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import gen, paper_1807_00399_b200 as cil
 

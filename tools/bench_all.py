@@ -84,7 +84,9 @@ for metric in ("point_to_plane", "point_to_point"):
     cil.profile_enable(False)
     r = cil.decode_result(res[:200])
     bpp = 24 if metric == "point_to_point" else 36
-    kern_us = 1e3 * st["acc_ms"] / max(st["n_acc"], 1)
+    # one cooperative persistent launch runs all iterations (per-iteration launches if the grid
+    # cannot be co-scheduled): per-iteration kernel time = launch time / iterations per launch
+    kern_us = 1e3 * st["acc_ms"] / max(st["n_acc"], 1) / (w3.max_iters if st["n_acc"] == 1 else 1)
     emit(config="C3_depth_projective", metric=metric, n_source=w3.m, n_target=w3.n, iterations=w3.max_iters,
          run_ms=ms, ms_per_iteration=ms / w3.max_iters, pairs_per_s=w3.m * w3.max_iters / (ms / 1e3),
          hbm_frac=bpp * w3.m / (ms / w3.max_iters * 1e-3) / 1e9 / PEAK, kernel_us=kern_us,

@@ -265,6 +265,7 @@ def run_ours(args, rank, world, local_rank):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_pair": bpp, "peak_source": peak_src,
                      "frac_of_8TBps_nominal": achieved / 8000.0},
+        "roofline_issue": _issue_roofline_from_profiles(),
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -287,6 +288,35 @@ def _traffic_from_profiles(workload):
         with open(p) as f:
             t = json.load(f).get(workload)
         return None if t is None else t.get("steady_iteration_bytes")
+    except Exception:
+        return None
+
+
+def _issue_roofline_from_profiles():
+    """the search kernel's instruction-issue roofline on a full-search iteration, from the
+    committed ncu --set full capture (profiles/r1_ncu_nn_it3_c4cert.txt): executed
+    warp-instructions / duration against 148 SMs x 4 schedulers x sm_max_mhz"""
+    p = os.path.join(ROOT, "profiles", "r1_ncu_nn_it3_c4cert.txt")
+    try:
+        vals = {}
+        for line in open(p):
+            parts = line.split()
+            if line.strip().startswith("Duration"):
+                vals["us"] = float(parts[1]) * (1e-3 if parts[2] == "ns" else 1.0)
+            elif line.strip().startswith("Executed Instructions"):
+                vals["inst"] = float(parts[2])
+            elif line.strip().startswith("Issue Slots Busy"):
+                vals["busy"] = float(parts[3]) / 100.0
+        mhz = 1965.0
+        try:
+            mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        except Exception:
+            pass
+        ach = vals["inst"] / (vals["us"] * 1e-6)
+        peak = 148 * 4 * mhz * 1e6
+        return {"bound": "issue", "kernel": "icp_nn_kernel, full-search iteration (ncu --set full capture)",
+                "achieved": ach, "peak": peak, "unit": "warp-instructions/s", "frac": ach / peak,
+                "ncu_issue_slots_busy": vals.get("busy"), "source": "profiles/r1_ncu_nn_it3_c4cert.txt"}
     except Exception:
         return None
 

@@ -247,7 +247,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {
             "workload": f"{w.name}: BASELINE.json configs[3] LiDAR 64x31250, {metric}, {iters} iterations, "
                         f"max dist {w.max_dist} m (target build + ICP run per step)",
-            "n_target": w.n, "n_source": w.m, "iterations": iters, "leaf_size": args.leaf or 8,
+            "n_target": w.n, "n_source": w.m, "iterations": iters, "leaf_size": args.leaf or 16,
             "l2": "flushed before every step (512 MiB device write)",
             "build_ms": build_ms / args.steps, "icp_ms_per_iteration": it_ms,
             "icp_select_kernel_ms": sel_ms, "icp_nn_kernel_ms": nn_ms, "icp_acc_kernel_ms": acc_ms,

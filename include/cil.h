@@ -70,7 +70,7 @@ typedef enum {
 typedef struct cil_target cil_target;   /* opaque, immutable after build */
 
 /* Spatial-index parameters (NULL = defaults).  leaf_size: points per BVH leaf
-   (0 = default 8; 1..32).  Other fields reserved, must be 0. */
+   (0 = default 16; 4, 8, 16 or 32).  Other fields reserved, must be 0. */
 typedef struct {
     int32_t leaf_size;
     int32_t reserved[7];
@@ -302,7 +302,7 @@ cil_status cil_debug_set_flags(uint32_t flags);   /* bits 1-2 engine debug mode,
    (sqrt(best) + g)^2 with g = clamp(kappa * (p's displacement in the last iteration),
    min_frac * max_corr_dist, max_frac * max_corr_dist), so that its match is certified (leaf /
    candidate list) while p moves less than about g / 2 (a point moving faster than
-   8 max_frac * max_corr_dist / kappa per iteration uses the minimum).  Defaults 0.001, 0.006, 16.
+   8 max_frac * max_corr_dist / kappa per iteration uses the minimum).  Defaults 0.001, 0.005, 16.
    0 <= min_frac <= max_frac <= 1, kappa >= 0.  Host-only, process-wide. */
 cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kappa);
 

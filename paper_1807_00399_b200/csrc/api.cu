@@ -24,7 +24,7 @@ int* g_trace = nullptr;
 }
 int* debug_trace() { return g_trace; }
 namespace {
-double g_skin_min = 0.001, g_skin_max = 0.006, g_skin_kappa = 16.0;
+double g_skin_min = 0.001, g_skin_max = 0.005, g_skin_kappa = 16.0;
 }
 void cert_skin_params(double* gmin, double* gmax, double* kappa) {
     *gmin = g_skin_min;

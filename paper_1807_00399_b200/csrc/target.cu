@@ -444,7 +444,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     if (n == 0) { set_error("cil_target_build: empty target (n == 0)"); return CIL_ERR_EMPTY_TARGET; }
     if (n < 0 || n > INT32_MAX) { set_error("cil_target_build: n=%lld out of range", (long long)n); return CIL_ERR_INVALID_ARG; }
     if (!pts) { set_error("cil_target_build: pts is NULL"); return CIL_ERR_INVALID_ARG; }
-    int B = 8;
+    int B = 16;                 // default leaf size (measured over C1-C5)
     if (params) {
         if (params->leaf_size) B = params->leaf_size;
         for (int k = 0; k < 7; ++k)

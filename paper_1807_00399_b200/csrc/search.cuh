@@ -311,7 +311,7 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 constexpr int kFrontierCap = CIL_FRONTIER_CAP;
 constexpr int kItemCap = 256;
 #ifndef CIL_DGROUP
-#define CIL_DGROUP 4
+#define CIL_DGROUP 2
 #endif
 #ifndef CIL_TRACE_D
 #define CIL_TRACE_D 1

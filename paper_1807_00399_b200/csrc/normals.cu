@@ -55,15 +55,10 @@ __device__ __forceinline__ void offer_leaf(const TargetView& T, const NegQuery& 
     float d2[B];
     leaf_d2<B>(T, nq, leaf, d2);
     const int* ids = reinterpret_cast<const int*>(T.leafsoa + (size_t)leaf * B + 3 * (B / 4));
-    // the k-th key is re-read only after an insertion (it can only shrink)
-    unsigned long long thr = kth(top, k);
-#pragma unroll 8
+#pragma unroll
     for (int c = 0; c < B; ++c) {
         const unsigned long long key = make_key(d2[c], (uint32_t)__ldg(ids + c));
-        if (key < thr) {                                    // (padding: d2 = +inf, never inserted)
-            topk_insert(top, key);
-            thr = kth(top, k);
-        }
+        if (key < kth(top, k)) topk_insert(top, key);      // (padding: d2 = +inf, never inserted)
     }
 }
 

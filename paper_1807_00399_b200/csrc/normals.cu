@@ -55,10 +55,27 @@ __device__ __forceinline__ void offer_leaf(const TargetView& T, const NegQuery& 
     float d2[B];
     leaf_d2<B>(T, nq, leaf, d2);
     const int* ids = reinterpret_cast<const int*>(T.leafsoa + (size_t)leaf * B + 3 * (B / 4));
+    // candidates that can enter the top k (d2 at most the k-th distance; padding d2 = +inf never
+    // does) as a bit mask, then ONE insertion site for them, lowest slot first (the order of the
+    // per-candidate test it replaces); a candidate's d2 is recomputed from the leaf with the same
+    // operations as leaf_d2, so no array is indexed at run time
+    unsigned long long thr = kth(top, k);
+    unsigned mask = 0;
 #pragma unroll
-    for (int c = 0; c < B; ++c) {
-        const unsigned long long key = make_key(d2[c], (uint32_t)__ldg(ids + c));
-        if (key < kth(top, k)) topk_insert(top, key);      // (padding: d2 = +inf, never inserted)
+    for (int c = 0; c < B; ++c) mask |= (d2[c] <= key_d2(thr) ? 1u : 0u) << c;
+    const float* row = reinterpret_cast<const float*>(T.leafsoa + (size_t)leaf * B);
+#pragma unroll 1
+    while (mask) {
+        const int c = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float2 x = make_float2(__ldg(row + c), 0.0f), y = make_float2(__ldg(row + B + c), 0.0f),
+                     z = make_float2(__ldg(row + 2 * B + c), 0.0f);
+        const float dc = pair_d2(nq, x, y, z).x;
+        const unsigned long long key = make_key(dc, (uint32_t)__ldg(ids + c));
+        if (key < thr) {
+            topk_insert(top, key);
+            thr = kth(top, k);
+        }
     }
 }
 

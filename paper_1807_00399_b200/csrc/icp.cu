@@ -42,6 +42,9 @@ constexpr int kIcpThreads = 256;
 // a point whose kappa x last-step displacement exceeds kSkinCut x gap_max searches with the
 // minimal skin (it would not keep a certificate anyway)
 constexpr float kSkinCut = CIL_SKIN_CUT;
+#ifndef CIL_KD_WARP_SOLVE
+#define CIL_KD_WARP_SOLVE true   // the last-CTA solve of the kd path by one warp (solve6_warp)
+#endif
 #ifndef CIL_RHO
 #define CIL_RHO 1.1           // certificate search bound rho = CIL_RHO x max_corr_dist
 #endif
@@ -1127,7 +1130,7 @@ icp_acc_kernel(const IterArgs a) {
             if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2, a.w_pp, a.w_pl);
     }
 
-    reduce_finalize<METRIC>(a, acc, Psh);
+    reduce_finalize<METRIC, CIL_KD_WARP_SOLVE>(a, acc, Psh);
 }
 
 // ---------------------------------------------------------------- K_proj
@@ -1367,7 +1370,7 @@ icp_shard_finish_kernel(const IterArgs a, const double* __restrict__ sums) {
     if (threadIdx.x < 16) Psh[threadIdx.x] = a.st->pose[threadIdx.x];
     if (threadIdx.x < kSlots) Ssum[threadIdx.x] = sums[threadIdx.x];
     __syncthreads();
-    solve_tail<METRIC>(a, Ssum, Psh);
+    solve_tail<METRIC, CIL_KD_WARP_SOLVE>(a, Ssum, Psh);
 }
 
 __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; }

@@ -445,6 +445,9 @@ constexpr int kSelThreads = 256;
 #endif
 constexpr int kSelRounds = CIL_SEL_ROUNDS;
 constexpr int kSelTile = kSelThreads * kSelRounds;     // 1024 queries per CTA
+#ifndef CIL_SEL_PERSIST
+#define CIL_SEL_PERSIST 1
+#endif
 
 // Certificates of query i at the current pose, one query per lane, the
 // whole warp together: returns true if the lane's query needs a full search; otherwise its
@@ -657,12 +660,20 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
     }
 }
 
+#if CIL_SEL_PERSIST
+#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads, 3)
+#else
+#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads)
+#endif
 template <int B>
-__global__ void __launch_bounds__(kSelThreads)
+__global__ void CIL_SEL_BOUNDS
 icp_select_kernel(const IterArgs a) {
     __shared__ SelWarp s_w[kSelThreads / 32];
     __shared__ double s_pose[12];
     __shared__ int s_cnt, s_np, s_base;
+#if !CIL_SEL_PERSIST
+    __shared__ int s_tile;
+#endif
     __shared__ int s_pk[kSelTile / 32];
     pdl_trigger();
     pdl_wait();
@@ -672,16 +683,31 @@ icp_select_kernel(const IterArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t kslot = (uint32_t)(*(volatile int*)&a.st->iters) & (kAnchorSlots - 1);
     if (threadIdx.x < 12) s_pose[threadIdx.x] = a.st->pose[threadIdx.x];
+    __syncthreads();
+    Pose34 P;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) P.r[e] = s_pose[e];
+#if CIL_SEL_PERSIST
+    // persistent: tiles of 1024 points claimed from a counter (no wave quantisation)
+    __shared__ int s_tile;
+    const int ntiles = (a.m + kSelTile - 1) / kSelTile;
+    for (;;) {
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&a.st->sel_work, 1u);
+#else
+    {
+    if (threadIdx.x == 0) s_tile = blockIdx.x;
+#endif
     if (threadIdx.x == 0) { s_cnt = 0; s_np = 0; }
     if ((threadIdx.x & 31) == 0) {
         SelWarp& S0 = s_w[threadIdx.x >> 5];
         S0.npc = 0; S0.nleaf = 0; S0.nlist = 0; S0.nitems = 0;
     }
     __syncthreads();
-    Pose34 P;
-#pragma unroll
-    for (int e = 0; e < 12; ++e) P.r[e] = s_pose[e];
-    const int wbase = blockIdx.x * kSelTile + warp * (32 * kSelRounds);
+    const int tile = s_tile;
+#if CIL_SEL_PERSIST
+    if (tile >= ntiles) break;
+#endif
+    const int wbase = tile * kSelTile + warp * (32 * kSelRounds);
     int cnt = 0, nrec = 0;
     SelIn in[kSelRounds];                    // every round's loads in flight together
 #pragma unroll
@@ -717,6 +743,8 @@ icp_select_kernel(const IterArgs a) {
     }
     __syncthreads();
     if (threadIdx.x < s_np) a.plist[s_base + threadIdx.x] = s_pk[threadIdx.x];
+    __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------- K_nn
@@ -1012,6 +1040,7 @@ __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[
         if (threadIdx.x == 0) {
             a.st->ticket = 0;
             a.st->work = 0;
+            a.st->sel_work = 0;
             a.st->searched += a.run ? a.st->list_n : 0;
             a.st->list_n = 0;
             a.st->plist_n = 0;
@@ -1047,6 +1076,7 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
         }
         a.st->ticket = 0;
         a.st->work = 0;      // K_nn's counter, for the next iteration
+        a.st->sel_work = 0;  // K_sel's tile counter
         a.st->searched += a.run ? a.st->list_n : 0;
         a.st->list_n = 0;
         a.st->plist_n = 0;
@@ -1339,6 +1369,7 @@ __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, 
         for (int i = 0; i < 16; ++i) st->pose[i] = pose_init[i];
         st->rmse = 0.0; st->n_corr = 0; st->iters = 0; st->converged = 0; st->status = CIL_OK;
         st->done = 0; st->ticket = 0; st->work = 0; st->list_n = 0; st->searched = 0; st->plist_n = 0;
+        st->sel_work = 0;
         st->pcert_n = 0; st->rec_leaf = 0; st->rec_list = 0; st->rec_items = 0;
         st->bar_count = 0; st->bar_gen = 0;
     }
@@ -1373,7 +1404,7 @@ icp_shard_finish_kernel(const IterArgs a, const double* __restrict__ sums) {
     solve_tail<METRIC, CIL_KD_WARP_SOLVE>(a, Ssum, Psh);
 }
 
-__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; }
+__global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; st->sel_work = 0; }
 
 template <class... KArgs, class... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
@@ -1443,7 +1474,11 @@ cudaError_t launch_iter(const IterArgs& a0, int metric, cudaStream_t s) {
     cudaError_t e0 = cudaSuccess;
     int n = 2;
     if (a.cert) {
-        const int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
+        int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
+#if CIL_SEL_PERSIST
+        static const int occ_sel = occupancy_of(icp_select_kernel<16>, kSelThreads);
+        g = std::min(g, occ_sel * sm_count());
+#endif
         prof_begin(kProfSel, s);
         switch (a.T.leaf_size) {
             case 4: e0 = launch_pdl(icp_select_kernel<4>, g, kSelThreads, s, a); break;

@@ -67,6 +67,7 @@ struct alignas(256) IcpState {
     long long rec_items;  // 208: leaves of those lists beyond the first
     unsigned int bar_count;  // 216: grid barrier of the persistent projective loop
     unsigned int bar_gen;    // 220
+    unsigned int sel_work;   // 224: tile counter of the persistent certificate kernel
 };
 
 // Certified warm start: anchor-pose ring of cil_icp_run.

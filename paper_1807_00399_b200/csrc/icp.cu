@@ -101,8 +101,6 @@ struct IterArgs {
 // (its dependent may be scheduled once every CTA of it has started) and pdl_wait() before it
 // reads anything an earlier kernel wrote (the wait returns when the previous grid has
 // completed and flushed), so the launch latency of kernel k+1 overlaps the tail of kernel k.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // diagnostics: %globaltimer stamp k of the running iteration (first = earliest CTA)
 __device__ __forceinline__ void stamp(const IterArgs& a, int k, bool first) {
@@ -1405,21 +1403,6 @@ icp_shard_finish_kernel(const IterArgs a, const double* __restrict__ sums) {
 }
 
 __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0; st->list_n = 0; st->sel_work = 0; }
-
-template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)block);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
 
 template <class K>
 int occupancy_of(K kernel, int threads) {

@@ -101,6 +101,30 @@ void prof_end(cudaStream_t s);              // records the end event
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Programmatic dependent launch: kernels of a dependent chain are launched with the
+// programmatic-stream-serialization attribute (launch_pdl); each calls pdl_trigger() first (its
+// dependent may be scheduled once every CTA of it has started) and pdl_wait() before it reads
+// anything an earlier kernel wrote (the wait returns when the previous grid has completed and
+// flushed), so the launch latency of kernel k+1 overlaps the tail of kernel k.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() { pdl_trigger(); pdl_wait(); }
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // target.cu: Morton order of a point set (perm: sorted position -> original index, sorted: the
 // points in that order, packed xyz); n >= 1
 cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* sorted, cudaStream_t s, int* nlaunch);

@@ -370,3 +370,12 @@ def test_normals_c3_config(cil):
     w = gen.c3_depth()
     frac = _check_normals(cil, w.target, 10, (0.0, 0.0, 0.0))
     assert frac > 0.95
+
+
+def test_run_empty_source(cil):
+    """cil_icp_run with m = 0: CIL_NO_CORRESPONDENCES after one iteration, identity pose"""
+    w = W.c1()
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    empty = torch.empty((0, 3), dtype=torch.float32, device="cuda")
+    res = cil.decode_result(cil.cil_icp_run(t, empty, dev(np.eye(4)), cil.make_params("point_to_plane", 5, 0.1))[0])
+    assert res.status == cil.CIL_NO_CORRESPONDENCES and res.iterations == 1 and np.array_equal(res.pose, np.eye(4))

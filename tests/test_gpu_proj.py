@@ -219,3 +219,21 @@ def test_proj_run_c3_from_ground_truth_and_deterministic(cil):
     a = [cil.decode_result(cil.cil_proj_run(dev(w.target), dev(w.target_normals), K, dev(w.source), dev(np.eye(4)),
                                             prm)[0]).pose for _ in range(2)]
     assert np.array_equal(a[0], a[1])
+
+
+def test_proj_run_empty_source_and_convergence_stop(cil):
+    """the persistent loop with an empty source stops at iteration 1 with CIL_NO_CORRESPONDENCES;
+    with convergence tolerances it stops at the oracle's iteration with the oracle's pose"""
+    w = W.c3()
+    K = cil.make_intrinsics(*C3_INTR)
+    empty = torch.empty((0, 3), dtype=torch.float32, device="cuda")
+    res = cil.decode_result(cil.cil_proj_run(dev(w.target), dev(w.target_normals), K, empty, dev(np.eye(4)),
+                                             cil.make_params("point_to_plane", 5, 0.05))[0])
+    assert res.status == cil.CIL_NO_CORRESPONDENCES and res.iterations == 1 and np.array_equal(res.pose, np.eye(4))
+    prm = cil.make_params("point_to_plane", 300, 0.05, rot_tol=1e-5, trans_tol=1e-5)
+    res = cil.decode_result(cil.cil_proj_run(dev(w.target), dev(w.target_normals), K, dev(w.source), dev(np.eye(4)),
+                                             prm)[0])
+    o = oracle.proj_run(w.target, w.target_normals, C3_INTR, w.source, "point_to_plane", 300, 0.05,
+                        rot_tol=1e-5, trans_tol=1e-5)
+    assert res.converged and o.converged and abs(res.iterations - o.iterations) <= 1
+    assert W.rot_angle(res.pose[:3, :3] @ o.pose[:3, :3].T) <= 1e-4 and np.abs(res.pose[:3, 3] - o.pose[:3, 3]).max() <= 1e-5

@@ -69,11 +69,27 @@ typedef enum {
 
 typedef struct cil_target cil_target;   /* opaque, immutable after build */
 
+/* Spatial index kinds (BASELINE.json north_star (2): "a uniform grid or Morton-sorted cells
+   ... or a GPU-traversable kd-tree, chosen by measurement"; DESIGN.md 4.1b has the table). */
+typedef enum {
+    CIL_INDEX_BVH = 0,     /* Morton-sorted leaves + implicit binary BVH (default; every path) */
+    CIL_INDEX_GRID = 1     /* the BVH plus a uniform grid (cells sized for grid_points targets per
+                              cell from the bounding box; capped at 2n cells): cil_nn_query and the
+                              stateless cil_icp_iterate search the grid (shells of cells, exact;
+                              lanes still unresolved after 2 shells finish on the BVH); the
+                              certified loop (cil_icp_run, shards) keeps the BVH.  Fastest when the
+                              target fills its bounding box and queries lie inside it (C2) */
+} cil_index_kind;
+
 /* Spatial-index parameters (NULL = defaults).  leaf_size: points per BVH leaf
-   (0 = default 16; 4, 8, 16 or 32).  Other fields reserved, must be 0. */
+   (0 = default 16; 4, 8, 16 or 32).  index_kind: cil_index_kind.  grid_points: mean target
+   points per grid cell over the bounding box (0 = default 2; CIL_INDEX_GRID only; > 0 and
+   finite).  Other fields reserved, must be 0. */
 typedef struct {
     int32_t leaf_size;
-    int32_t reserved[7];
+    int32_t index_kind;
+    float grid_points;
+    int32_t reserved[5];
 } cil_index_params;
 
 /* ICP parameters.  metric: cil_metric.  max_iters >= 1 (cil_icp_run only).
@@ -128,6 +144,8 @@ typedef struct {
     int32_t leaf_size;
     int32_t has_normals;
     int64_t device_bytes; /* bytes owned by the target */
+    int32_t index_kind;   /* cil_index_kind it was built with */
+    int32_t pad;
 } cil_target_info;
 
 /* Build the spatial index over the target (BASELINE.json north_star

@@ -37,6 +37,8 @@ CIL_ERR_OOM = 5
 CIL_ERR_WORKSPACE = 6
 CIL_ERR_DEGENERATE = 16
 CIL_NO_CORRESPONDENCES = 17
+CIL_INDEX_BVH = 0
+CIL_INDEX_GRID = 1
 CIL_POINT_TO_POINT = 0
 CIL_POINT_TO_PLANE = 1
 CIL_COMBINED = 2
@@ -52,7 +54,8 @@ EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_n
 
 
 class cil_index_params(C.Structure):
-    _fields_ = [("leaf_size", C.c_int32), ("reserved", C.c_int32 * 7)]
+    _fields_ = [("leaf_size", C.c_int32), ("index_kind", C.c_int32), ("grid_points", C.c_float),
+                ("reserved", C.c_int32 * 5)]
 
 
 class cil_icp_params(C.Structure):
@@ -91,7 +94,8 @@ def make_intrinsics(width: int, height: int, fx: float, fy: float, cx: float, cy
 
 class cil_target_info(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_leaves", C.c_int64), ("n_nodes", C.c_int64), ("leaf_size", C.c_int32),
-                ("has_normals", C.c_int32), ("device_bytes", C.c_int64)]
+                ("has_normals", C.c_int32), ("device_bytes", C.c_int64), ("index_kind", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 _vp, _i64, _sz = C.c_void_p, C.c_int64, C.c_size_t
@@ -275,7 +279,7 @@ class Target:
 
 
 def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, leaf_size: int = 0,
-                     stream=None) -> Target:
+                     stream=None, index: str = "bvh", grid_points: float = 0.0) -> Target:
     _pts(pts, "pts")
     if normals is not None:
         _pts(normals, "normals")
@@ -283,6 +287,8 @@ def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, lea
             raise ValueError("normals must match pts")
     prm = cil_index_params()
     prm.leaf_size = int(leaf_size)
+    prm.index_kind = {"bvh": CIL_INDEX_BVH, "grid": CIL_INDEX_GRID}[index]
+    prm.grid_points = float(grid_points)
     h = _vp()
     _check(_lib.cil_target_build(_ptr(pts), _ptr(normals), pts.shape[0], C.byref(prm), _stream_ptr(stream),
                                  C.byref(h)), "cil_target_build")

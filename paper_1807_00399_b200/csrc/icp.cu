@@ -28,6 +28,7 @@
 // cil_icp_iterate = K_nn over all points (no hints, bound max_corr_dist) + K_acc.
 #include "internal.cuh"
 #include "search.cuh"
+#include "grid.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -888,6 +889,28 @@ icp_nn_kernel(const IterArgs a) {
     nn_packet_engine<B, CERT>(a.T, qs, a.m, &a.st->work);
 }
 
+// K_nn on the grid index (CIL_INDEX_GRID, stateless cil_icp_iterate only): one source point
+// per thread, a1 transform (double-float) + exact grid search bounded by max_corr_dist
+template <int B>
+__global__ void __launch_bounds__(kNNThreads)
+icp_grid_nn_kernel(const IterArgs a) {
+    pdl_trigger();
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.m) return;
+    Pose34 P;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.r[k] = __ldg(a.pose_in + k);
+    const DF3 s = transform_df(P, a.src[3 * (size_t)i], a.src[3 * (size_t)i + 1], a.src[3 * (size_t)i + 2]);
+    const unsigned long long none = bound_key(a.search2);
+    const unsigned long long best = grid_search<B, true>(a.T, s, none);
+    const bool found = best != none;
+    a.nn[i] = found ? (int)key_idx(best) : -1;
+    const size_t o = a.perm[i];
+    if (a.corr_idx) a.corr_idx[o] = found ? (int32_t)key_idx(best) : -1;
+    if (a.corr_d2) a.corr_d2[o] = found ? key_d2(best) : INFINITY;
+}
+
 // a1 + a3 + a4 + a5 for the pair (p, t): transform, inclusive rejection (R2), residual,
 // Jacobian, fp32 per-thread sums (29 point-to-plane / 17 point-to-point values)
 // (accumulate_s: the same for an already transformed s; returns whether the pair was accepted
@@ -1430,8 +1453,24 @@ cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
     return e;
 }
 
+template <int B>
+cudaError_t launch_grid_nn_b(const IterArgs& a, cudaStream_t s) {
+    prof_begin(kProfNN, s);
+    cudaError_t e = launch_pdl(icp_grid_nn_kernel<B>, std::max(1, (a.m + kNNThreads - 1) / kNNThreads), kNNThreads, s, a);
+    prof_end(s);
+    return e;
+}
+
 template <bool CERT>
 cudaError_t launch_nn_t(const IterArgs& a, cudaStream_t s) {
+    if (!CERT && !a.run && a.T.gpts) {             // stateless iterate on the grid index
+        switch (a.T.leaf_size) {
+            case 4: return launch_grid_nn_b<4>(a, s);
+            case 8: return launch_grid_nn_b<8>(a, s);
+            case 16: return launch_grid_nn_b<16>(a, s);
+            default: return launch_grid_nn_b<32>(a, s);
+        }
+    }
     switch (a.T.leaf_size) {
         case 4: return launch_nn_b<4, CERT>(a, s);
         case 8: return launch_nn_b<8, CERT>(a, s);

@@ -19,6 +19,17 @@ constexpr int kSlots = 32;
 // Morton bits per axis (48-bit keys -> 6 radix passes of 8 bits).
 constexpr int kMortonBits = 16;
 
+// Uniform grid over the target (index_kind CIL_INDEX_GRID; grid.cu): cell size and dimensions
+// are chosen on the device from the bounding box, so the kernels read them from this
+// descriptor.  Cell (cx, cy, cz) has the x-major linear id (cz * ny + cy) * nx + cx; a point p
+// is in cell clamp(floor((p - lo) * inv_h), 0, n - 1) per axis.  eps bounds the rounding of
+// that assignment: every point of cell c lies in [lo + c h - eps, lo + (c + 1) h + eps].
+struct GridDesc {
+    float4 lo_h;          // lo.x, lo.y, lo.z, h
+    float4 inv_eps;       // inv_h, eps, 0, 0
+    int4 dims;            // nx, ny, nz, nx * ny * nz
+};
+
 // The target, as the kernels see it (device pointers + sizes).  Passed by value.
 struct TargetView {
     const float4* opts;   // [n] ORIGINAL order: x, y, z, __int_as_float(sorted position)
@@ -34,6 +45,9 @@ struct TargetView {
     int levels;           // log2(l_pad)
     int leaf_size;
     int coarse_bits;      // multiple of 3, <= 21
+    const float4* gpts;   // grid: [n] points sorted by cell (x, y, z, original index bits), or nullptr
+    const uint32_t* gstart;  // grid: [cells + 1] first sorted position of every cell
+    const GridDesc* gdesc;   // grid: descriptor (device)
     int* trace;           // diagnostics only (cil_debug_engine_trace), normally nullptr
     int dbg_mode;         // diagnostics only (cil_debug_set_flags bits 1-2), normally 0
 };
@@ -42,8 +56,10 @@ struct cil_target {
     TargetView v;
     int64_t n_leaves;
     int has_normals;
+    int index_kind;       // CIL_INDEX_BVH or CIL_INDEX_GRID (BVH + grid)
     int device;
     void* mem;            // single stream-ordered allocation holding pts / nrm / box
+    void* gmem;           // the grid's allocation (CIL_INDEX_GRID) or nullptr
     size_t bytes;
 };
 
@@ -133,6 +149,11 @@ cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* 
 size_t radix_sort_scratch_bytes(int n);
 cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long long* k1, uint32_t* v1, int n,
                              int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt);
+
+// grid.cu: the uniform grid of a target (after its BVH build; quant = bbox min, qmax = bbox max
+// written by the build); allocates from the pool into *mem (owned by the target afterwards)
+cudaError_t grid_build(const float* pts, int n, const float4* quant, const float4* qmax, float pts_per_cell,
+                       cudaStream_t s, void** mem, size_t* bytes, TargetView* v, int* nlaunch);
 
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);

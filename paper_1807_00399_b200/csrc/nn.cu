@@ -2,6 +2,7 @@
 // BASELINE.json configs[1]; "k-NN ... queries").
 #include "internal.cuh"
 #include "search.cuh"
+#include "grid.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -64,6 +65,19 @@ nn_query_kernel(TargetView T, NNQueries qs, int m, unsigned int* counter) {
     nn_packet_engine<B, false>(T, qs, m, counter);
 }
 
+// the grid index (CIL_INDEX_GRID): one query per thread, in the same Morton-cell order
+template <int B>
+__global__ void __launch_bounds__(kNNThreads)
+grid_query_kernel(TargetView T, NNQueries qs, int m) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    DF3 s;
+    unsigned long long best;
+    int hint;
+    qs.load(k, s, best, hint);
+    qs.store(k, grid_search<B, false>(T, s, best), 0.0f);
+}
+
 template <int B>
 cudaError_t launch_nn(const TargetView& T, const NNQueries& qs, int m, unsigned int* counter, cudaStream_t s) {
     static int occ = -1;   // per-process cache; all supported devices are sm_100a
@@ -77,6 +91,11 @@ cudaError_t launch_nn(const TargetView& T, const NNQueries& qs, int m, unsigned 
     TargetView Tv = T;
     Tv.trace = debug_trace();
     Tv.dbg_mode = (int)(debug_flags() >> 1) & 3;
+    if (T.gpts) {
+        grid_query_kernel<B><<<(int)(((int64_t)m + kNNThreads - 1) / kNNThreads), kNNThreads, 0, s>>>(Tv, qs, m);
+        count_launches(1);
+        return cudaGetLastError();
+    }
     nn_query_kernel<B><<<blocks, kNNThreads, 0, s>>>(Tv, qs, m, counter);
     count_launches(1);
     return cudaGetLastError();

@@ -83,6 +83,7 @@ __global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, floa
         const float ext = fmaxf(fmaxf(sm[3][0] - sm[0][0], sm[4][0] - sm[1][0]), sm[5][0] - sm[2][0]);
         const float cells = (float)((1 << kMortonBits) - 1);
         *quant = make_float4(sm[0][0], sm[1][0], sm[2][0], ext > 0.0f ? cells / ext : 0.0f);
+        quant[1] = make_float4(sm[3][0], sm[4][0], sm[5][0], 0.0f);      // the maximum (grid.cu)
     }
 }
 
@@ -445,10 +446,22 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     if (n < 0 || n > INT32_MAX) { set_error("cil_target_build: n=%lld out of range", (long long)n); return CIL_ERR_INVALID_ARG; }
     if (!pts) { set_error("cil_target_build: pts is NULL"); return CIL_ERR_INVALID_ARG; }
     int B = 16;                 // default leaf size (measured over C1-C5)
+    int kind = CIL_INDEX_BVH;
+    float grid_points = 2.0f;   // targets per grid cell
     if (params) {
         if (params->leaf_size) B = params->leaf_size;
-        for (int k = 0; k < 7; ++k)
+        kind = params->index_kind;
+        if (params->grid_points != 0.0f) grid_points = params->grid_points;
+        for (int k = 0; k < 5; ++k)
             if (params->reserved[k]) { set_error("cil_target_build: reserved index params must be 0"); return CIL_ERR_INVALID_ARG; }
+    }
+    if (kind != CIL_INDEX_BVH && kind != CIL_INDEX_GRID) {
+        set_error("cil_target_build: index_kind %d not supported", kind);
+        return CIL_ERR_INVALID_ARG;
+    }
+    if (!(grid_points > 0.0f) || !std::isfinite(grid_points)) {
+        set_error("cil_target_build: grid_points must be finite and > 0");
+        return CIL_ERR_INVALID_ARG;
     }
     if (B != 4 && B != 8 && B != 16 && B != 32) {
         set_error("cil_target_build: leaf_size %d not in {4, 8, 16, 32}", B);
@@ -539,13 +552,30 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
         first >>= lv;
         rem -= lv;
     }
+    TargetView gv{};
+    void* gmem = nullptr;
+    size_t gbytes = 0;
+    if (kind == CIL_INDEX_GRID && e == cudaSuccess) {
+        int ng = 0;
+        e = grid_build(pts, N, d_quant, d_quant + 1, grid_points, s, &gmem, &gbytes, &gv, &ng);
+        nlaunch += ng;
+    }
     count_launches(3 + 2 * ((3 * kMortonBits + kRadixBits - 1) / kRadixBits) + nlaunch + 4 + tree_passes);
     prof_end(s);
-    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     pool_free(tmp, s);
-    if (e != cudaSuccess) { pool_free(mem, s); return cuda_fail(e, "cil_target_build launch"); }
+    if (e != cudaSuccess) {
+        pool_free(mem, s);
+        if (gmem) pool_free(gmem, s);
+        return cuda_fail(e, "cil_target_build launch");
+    }
 
     cil_target* t = new cil_target;
+    t->v.gpts = gv.gpts;
+    t->v.gstart = gv.gstart;
+    t->v.gdesc = gv.gdesc;
+    t->gmem = gmem;
+    t->index_kind = kind;
     t->v.opts = d_pts;
     t->v.onrm = d_nrm;
     t->v.box = d_box;
@@ -565,7 +595,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     t->has_normals = normals ? 1 : 0;
     t->device = dev;
     t->mem = mem;
-    t->bytes = bytes;
+    t->bytes = bytes + gbytes;
     *out = t;
     return CIL_OK;
 }
@@ -573,6 +603,10 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
 CIL_API cil_status cil_target_free(cil_target* t, cil_stream_t stream) {
     if (!t) return CIL_OK;
     cudaError_t e = pool_free(t->mem, (cudaStream_t)stream);
+    if (t->gmem) {
+        const cudaError_t e2 = pool_free(t->gmem, (cudaStream_t)stream);
+        if (e == cudaSuccess) e = e2;
+    }
     delete t;
     if (e != cudaSuccess) return cuda_fail(e, "pool_free(target)");
     return CIL_OK;
@@ -586,5 +620,7 @@ CIL_API cil_status cil_target_get_info(const cil_target* t, cil_target_info* inf
     info->leaf_size = t->v.leaf_size;
     info->has_normals = t->has_normals;
     info->device_bytes = (int64_t)t->bytes;
+    info->index_kind = t->index_kind;
+    info->pad = 0;
     return CIL_OK;
 }

@@ -43,9 +43,10 @@ def test_struct_layouts_match_header(cil):
 int main(void) {
   printf("%zu %zu %zu %zu %zu %zu\n", sizeof(cil_index_params), sizeof(cil_icp_params), sizeof(cil_icp_result),
          sizeof(cil_icp_system), sizeof(cil_target_info), sizeof(cil_intrinsics));
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", offsetof(cil_icp_params, max_corr_dist), offsetof(cil_icp_result, rmse),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", offsetof(cil_icp_params, max_corr_dist), offsetof(cil_icp_result, rmse),
          offsetof(cil_icp_result, status), offsetof(cil_icp_system, sse), offsetof(cil_icp_system, status),
-         offsetof(cil_target_info, device_bytes), offsetof(cil_intrinsics, fx), offsetof(cil_intrinsics, cy));
+         offsetof(cil_target_info, device_bytes), offsetof(cil_intrinsics, fx), offsetof(cil_intrinsics, cy),
+         offsetof(cil_index_params, index_kind), offsetof(cil_index_params, grid_points), offsetof(cil_target_info, index_kind));
   return 0;
 }
 """
@@ -62,7 +63,9 @@ int main(void) {
     assert offs == [cil.cil_icp_params.max_corr_dist.offset, cil.cil_icp_result.rmse.offset,
                     cil.cil_icp_result.status.offset, cil.cil_icp_system.sse.offset,
                     cil.cil_icp_system.status.offset, cil.cil_target_info.device_bytes.offset,
-                    cil.cil_intrinsics.fx.offset, cil.cil_intrinsics.cy.offset]
+                    cil.cil_intrinsics.fx.offset, cil.cil_intrinsics.cy.offset,
+                    cil.cil_index_params.index_kind.offset, cil.cil_index_params.grid_points.offset,
+                    cil.cil_target_info.index_kind.offset]
 
 
 def test_host_side_argument_errors(cil):
@@ -77,6 +80,16 @@ def test_host_side_argument_errors(cil):
     bad.leaf_size = 7
     assert L.cil_target_build(C.c_void_p(256), None, 10, C.byref(bad), None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
     assert "leaf_size" in L.cil_last_error().decode()
+    bad = cil.cil_index_params()
+    bad.index_kind = 7
+    assert L.cil_target_build(C.c_void_p(256), None, 10, C.byref(bad), None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+    assert "index_kind" in L.cil_last_error().decode()
+    bad = cil.cil_index_params()
+    bad.index_kind = cil.CIL_INDEX_GRID
+    for gp in (-1.0, float("nan"), float("inf")):
+        bad.grid_points = gp
+        assert L.cil_target_build(C.c_void_p(256), None, 10, C.byref(bad), None, C.byref(h)) == cil.CIL_ERR_INVALID_ARG
+        assert "grid_points" in L.cil_last_error().decode()
     assert L.cil_nn_query(None, None, 10, 1.0, None, None, None) == cil.CIL_ERR_INVALID_ARG
     p = cil.make_params("point_to_plane", 10, 0.1)
     assert L.cil_icp_iterate(None, None, 10, None, C.byref(p), None, 0, None, None, None, None, None) == \

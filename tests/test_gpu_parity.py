@@ -65,13 +65,17 @@ def check_nn(tgt, queries_f64, g_idx, g_d2, o_idx, o_d2, max_d2=math.inf):
 
 
 # ------------------------------------------------------------------ NN
+INDEXES = ["bvh", "grid"]
+
+
+@pytest.mark.parametrize("index", INDEXES)
 @pytest.mark.parametrize("n,m,leaf", [(1, 5, 8), (7, 33, 8), (8, 64, 8), (9, 257, 4), (1000, 1000, 16),
                                       (4097, 3001, 32), (65537, 100003, 8)])
-def test_nn_small_ragged(cil, n, m, leaf):
+def test_nn_small_ragged(cil, n, m, leaf, index):
     rng = np.random.default_rng(n + m)
     T = rng.standard_normal((n, 3)).astype(np.float32)
     Q = (rng.standard_normal((m, 3)) * 1.1).astype(np.float32)
-    t = cil.cil_target_build(dev(T), None, leaf_size=leaf)
+    t = cil.cil_target_build(dev(T), None, leaf_size=leaf, index=index)
     gi, gd = cil.cil_nn_query(t, dev(Q))
     o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2)
     check_nn(T, Q.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2)
@@ -79,12 +83,13 @@ def test_nn_small_ragged(cil, n, m, leaf):
     assert info.n == n and info.leaf_size == leaf and info.n_leaves == (n + leaf - 1) // leaf
 
 
-def test_nn_ties_lowest_original_index(cil):
+@pytest.mark.parametrize("index", INDEXES)
+def test_nn_ties_lowest_original_index(cil, index):
     """R1: exact ties (duplicated integer grid points, cube centres) -> lowest original index."""
     g = np.stack(np.meshgrid(*[np.arange(10)] * 3, indexing="ij"), -1).reshape(-1, 3).astype(np.float32)
     T = np.concatenate([g[::-1], g, g[::-1]])
     Q = np.concatenate([g, g + 0.5, g + 0.25, g - 0.5]).astype(np.float32)
-    t = cil.cil_target_build(dev(T), None, leaf_size=4)
+    t = cil.cil_target_build(dev(T), None, leaf_size=4, index=index)
     gi, gd = cil.cil_nn_query(t, dev(Q))
     from scipy.spatial.distance import cdist
     D = cdist(Q.astype(np.float64), T.astype(np.float64), "sqeuclidean")
@@ -93,11 +98,12 @@ def test_nn_ties_lowest_original_index(cil):
     assert np.array_equal(gd.cpu().numpy().astype(np.float64), D[np.arange(len(Q)), ref])
 
 
-def test_nn_bounded_and_empty(cil):
+@pytest.mark.parametrize("index", INDEXES)
+def test_nn_bounded_and_empty(cil, index):
     rng = np.random.default_rng(1)
     T = rng.random((5000, 3)).astype(np.float32)
     Q = rng.random((7000, 3)).astype(np.float32)
-    t = cil.cil_target_build(dev(T), None)
+    t = cil.cil_target_build(dev(T), None, index=index)
     for md in (0.0, 0.01, 0.03):
         gi, gd = cil.cil_nn_query(t, dev(Q), max_dist=md)
         o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2, max_dist=md)
@@ -111,10 +117,47 @@ def test_nn_bounded_and_empty(cil):
     assert np.array_equal(gi.cpu().numpy(), np.arange(5000)) and (gd.cpu().numpy() == 0).all()
 
 
-def test_nn_c2_full_size(cil):
+@pytest.mark.parametrize("shape", ["point", "line", "plane", "far", "lidar_like"])
+def test_nn_grid_degenerate(cil, shape):
+    """The uniform grid on degenerate extents (all points equal, a line, a plane: flat axes get
+    one cell), queries far outside the bounding box (shells never reach: BVH fallback) and a
+    strongly non-uniform cloud -- against the oracle, both indexes."""
+    rng = np.random.default_rng(11)
+    n, m = 3000, 4000
+    if shape == "point":
+        T = np.tile(np.float32([[1.5, -2.0, 3.25]]), (n, 1))
+        Q = (rng.standard_normal((m, 3)) + [1.5, -2.0, 3.25]).astype(np.float32)
+    elif shape == "line":
+        T = np.stack([rng.random(n), np.zeros(n), np.zeros(n)], 1).astype(np.float32)
+        Q = rng.random((m, 3)).astype(np.float32)
+    elif shape == "plane":
+        T = np.stack([rng.random(n), rng.random(n), np.full(n, 0.5)], 1).astype(np.float32)
+        Q = rng.random((m, 3)).astype(np.float32)
+    elif shape == "far":
+        T = rng.random((n, 3)).astype(np.float32)
+        Q = (rng.standard_normal((m, 3)) * 50.0).astype(np.float32)
+    else:
+        r = np.exp(rng.uniform(0, 4, n))
+        a = rng.uniform(0, 2 * np.pi, n)
+        T = np.stack([r * np.cos(a), r * np.sin(a), rng.normal(0, 0.01, n)], 1).astype(np.float32)
+        Q = (T[rng.integers(0, n, m)] + rng.normal(0, 0.05, (m, 3))).astype(np.float32)
+    o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2)
+    res = []
+    for index in INDEXES:
+        t = cil.cil_target_build(dev(T), None, index=index)
+        gi, gd = cil.cil_nn_query(t, dev(Q))
+        check_nn(T, Q.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2)
+        assert t.info().index_kind == (cil.CIL_INDEX_GRID if index == "grid" else cil.CIL_INDEX_BVH)
+        res.append((gi.cpu().numpy(), gd.cpu().numpy()))
+    # both indexes return the same (exact) minimum of the same fp32 arithmetic
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("index", INDEXES)
+def test_nn_c2_full_size(cil, index):
     """BASELINE.json configs[1] at full size (2^20 x 2^20), every query checked."""
     w = W.c2()
-    t = cil.cil_target_build(dev(w.target), None)
+    t = cil.cil_target_build(dev(w.target), None, index=index)
     gi, gd = cil.cil_nn_query(t, dev(w.source))
     torch.cuda.synchronize()
     o_idx, o_d2 = oracle.knn(None, w.source.astype(np.float64), k=2, tree=W.oracle_tree(w))
@@ -147,10 +190,10 @@ def _params(cil, metric, iters, max_dist):
     return cil.make_params(metric, iters, max_dist)
 
 
-def check_iteration(cil, w, pose, metric, tree=None, sample=None, leaf=0):
+def check_iteration(cil, w, pose, metric, tree=None, sample=None, leaf=0, index="bvh"):
     """cil_icp_iterate vs oracle at the same pose_in: correspondences, H, g, pose_out."""
     t = cil.cil_target_build(dev(w.target), dev(w.target_normals) if w.target_normals is not None else None,
-                             leaf_size=leaf)
+                             leaf_size=leaf, index=index)
     prm = _params(cil, metric, 1, w.max_dist)
     P = dev(pose.astype(np.float64))
     pose_out, sys_t, ci, cd = cil.cil_icp_iterate(t, dev(w.source), P, prm, want_corr=True)
@@ -199,10 +242,32 @@ def test_iterate_c4_reduced(cil, metric):
         check_iteration(cil, w, _perturb(w.gt_pose, frac), metric)
 
 
-@pytest.mark.parametrize("logn", [16, 18])
+@pytest.mark.parametrize("logn", [16, 18, 20])
 def test_iterate_c5(cil, logn):
     w = W.c5(logn)
     check_iteration(cil, w, np.eye(4), "point_to_plane")
+
+
+@pytest.mark.parametrize("case", ["c1", "c4", "c5", "c3"])
+def test_iterate_grid_index(cil, case):
+    """The stateless iterate on the uniform-grid index (CIL_INDEX_GRID) against the oracle, and
+    bit-equal to the BVH path (both return the exact minimum of the same fp32 arithmetic; the
+    accumulation is the same kernel)."""
+    if case == "c1":
+        w, poses = W.c1(), None
+    elif case == "c4":
+        w, poses = W.c4("point_to_plane", rings=16, az=8000), None
+    elif case == "c5":
+        w, poses = W.c5(16), [np.eye(4)]
+    else:
+        w, poses = W.c3(), [np.eye(4)]
+    poses = poses or [_perturb(w.gt_pose, f) for f in (0.0, 0.5, 1.0)]
+    tree = W.oracle_tree(w)
+    for pose in poses:
+        gs, gi = check_iteration(cil, w, pose, "point_to_plane", tree=tree, index="grid")
+        bs, bi = check_iteration(cil, w, pose, "point_to_plane", tree=tree, index="bvh")
+        assert np.array_equal(gi, bi)
+        assert np.array_equal(gs.H, bs.H) and np.array_equal(gs.g, bs.g)
 
 
 def test_iterate_c3(cil):

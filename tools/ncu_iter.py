@@ -7,7 +7,7 @@ from scipy.spatial.transform import Rotation
 frac = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
 w = gen.c4_lidar("point_to_plane")
 d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
-t = cil.cil_target_build(d(w.target), d(w.target_normals), 8)
+t = cil.cil_target_build(d(w.target), d(w.target_normals))
 rv = Rotation.from_matrix(w.gt_pose[:3, :3]).as_rotvec() * frac
 T = np.eye(4); T[:3, :3] = Rotation.from_rotvec(rv).as_matrix(); T[:3, 3] = w.gt_pose[:3, 3] * frac
 prm = cil.make_params("point_to_plane", 1, 1.0)

@@ -6,7 +6,7 @@ import gen, paper_1807_00399_b200 as cil
 
 w = gen.c2_uniform()
 d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
-t = cil.cil_target_build(d(w.target), None, 8)
+t = cil.cil_target_build(d(w.target), None)
 q = d(w.source)
 f32 = lambda a: np.asarray(a, np.int32).view(np.float32)
 tr = torch.zeros(w.m * 16, dtype=torch.int32, device="cuda")

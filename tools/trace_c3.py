@@ -10,7 +10,7 @@ w = gen.c3_depth()
 d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
 t0 = cil.cil_target_build(d(w.target), None)
 nrm, _ = cil.cil_estimate_normals(t0, 10, (0.0, 0.0, 0.0))
-t = cil.cil_target_build(d(w.target), nrm, 8)
+t = cil.cil_target_build(d(w.target), nrm)
 src = d(w.source)
 f32 = lambda a: np.asarray(a, np.int32).view(np.float32)
 

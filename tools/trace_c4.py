@@ -9,7 +9,7 @@ from scipy.spatial.transform import Rotation
 metric = "point_to_plane"
 w = gen.c4_lidar(metric)
 d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
-t = cil.cil_target_build(d(w.target), d(w.target_normals), 8)
+t = cil.cil_target_build(d(w.target), d(w.target_normals))
 src = d(w.source)
 f32 = lambda a: np.asarray(a, np.int32).view(np.float32)
 

@@ -314,7 +314,7 @@ cil_status cil_profile_read(cil_profile_stats* out);
 
 /* Diagnostics: bit 0 set = cil_icp_run does a full search every iteration (no certified
    warm start); used to measure the certificate.  Host-only, process-wide. */
-cil_status cil_debug_set_flags(uint32_t flags);   /* bits 1-2 engine debug mode, bit 3 no point certificate, bit 4 caller order, bit 5 Morton order */
+cil_status cil_debug_set_flags(uint32_t flags);   /* bit 0 no certified warm start, bits 1-2 engine debug mode, bit 3 no point certificate, bit 4 caller order, bit 5 Morton order, bit 6 no small-problem brute-force path */
 
 /* Tuning: the certificate skin of cil_icp_run.  A full search of point p uses the threshold
    (sqrt(best) + g)^2 with g = clamp(kappa * (p's displacement in the last iteration),

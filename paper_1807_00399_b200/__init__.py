@@ -163,6 +163,13 @@ def set_certificates(on: bool = True) -> None:
     _check(_lib.cil_debug_set_flags(0 if on else 1), "cil_debug_set_flags")
 
 
+def set_debug_flags(flags: int) -> None:
+    """cil_debug_set_flags (diagnostics): bit 0 no certified warm start, bits 1-2 engine mode,
+    bit 3 no point certificate, bit 4 caller's source order, bit 5 Morton source order,
+    bit 6 no small-problem (brute-force) path"""
+    _check(_lib.cil_debug_set_flags(int(flags)), "cil_debug_set_flags")
+
+
 def set_cert_skin(min_frac: float = 0.001, max_frac: float = 0.005, kappa: float = 16.0) -> None:
     """certificate skin of cil_icp_run: g = clamp(kappa * last-step displacement, min, max) x max_corr_dist"""
     _check(_lib.cil_debug_set_cert_skin(float(min_frac), float(max_frac), float(kappa)), "cil_debug_set_cert_skin")

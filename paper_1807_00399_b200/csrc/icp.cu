@@ -986,6 +986,7 @@ __device__ __forceinline__ void accumulate_pair(float (&acc)[kSlots], const Pose
 
 // Per-CTA partial of the 32 fp32 per-thread sums: warp transpose-reduce (fp32) -> per-warp fp64
 // -> fixed-order sum over the warps -> partials[slot * kMaxCtas + blockIdx.x] (slot-major)
+template <int NW = kIcpWarps>
 __device__ __forceinline__ void cta_partial(float (&acc)[kSlots], double (*wsum)[kSlots], double* partials) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float mine = warp_transpose_reduce(acc);
@@ -994,7 +995,7 @@ __device__ __forceinline__ void cta_partial(float (&acc)[kSlots], double (*wsum)
     if (threadIdx.x < kSlots) {
         double v = 0.0;
 #pragma unroll
-        for (int w = 0; w < kIcpWarps; ++w) v += wsum[w][threadIdx.x];
+        for (int w = 0; w < NW; ++w) v += wsum[w][threadIdx.x];
         partials[(size_t)threadIdx.x * kMaxCtas + blockIdx.x] = v;
         __threadfence();
     }
@@ -1006,6 +1007,7 @@ __device__ __forceinline__ void cta_partial(float (&acc)[kSlots], double (*wsum)
 // a fixed function of G: bitwise reproducible, and identical in every CTA that runs it).
 __device__ __forceinline__ void sum_partials(const double* partials, int G, double* Ssum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp >= 8) return;                        // (CTAs of more than 8 warps: the first 8 sum)
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int b0 = 0; b0 < G; b0 += 4 * 32) {
         double xv[4][4];
@@ -1036,13 +1038,13 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
 // Epilogue of the accumulation kernels: warp transpose-reduce (fp32) -> per-warp fp64 ->
 // per-CTA partial; the last CTA (ticket) sums the partials in fixed order, solves, updates
 // the pose and (certified run) writes the anchor table of the next iteration.
-template <int METRIC, bool WARP = false>
+template <int METRIC, bool WARP = false, int NW = kIcpWarps>
 __device__ __forceinline__ void reduce_finalize(const IterArgs& a, float (&acc)[kSlots], const double* Psh) {
-    __shared__ double wsum[kIcpWarps][kSlots];
+    __shared__ double wsum[NW][kSlots];
     __shared__ double Ssum[kSlots];
     __shared__ int last;
     // ---- reductions (a5): warp transpose-reduce (fp32) -> per-warp fp64 -> per-CTA partial
-    cta_partial(acc, wsum, a.partials);
+    cta_partial<NW>(acc, wsum, a.partials);
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
     __syncthreads();
@@ -1382,6 +1384,187 @@ icp_proj_run_kernel(const IterArgs a, int iters) {
     }
 }
 
+// ---------------------------------------------------------------- small problems (brute force)
+// A target of at most kSmallMaxN points fits in shared memory, and for m * n <= kSmallMaxPairs
+// the exact 1-NN by brute force (every target, u64 key minimum: R1 ties) costs a few
+// microseconds spread over the whole GPU, while a tree search of a few thousand queries is
+// bound by the latency of one warp's traversal (C1: ~25 us per iteration).  Each query is
+// taken by a group of G lanes (G = a power of two chosen so that m * G fills the grid); lane k
+// of the group scans targets k, k + G, ...; the group reduces its keys by shuffles and the
+// group leader accumulates the pair (a3-a5), so the iteration is ONE launch (iterate) or the
+// whole loop is one cooperative persistent launch (run: grid barrier, every CTA sums the
+// partials in the same fixed order and solves redundantly, as the projective loop does; the
+// same grid, assignment and reduction as the iterate kernel, so run == chained iterates bit for
+// bit).  The source is used in the caller's order (no Morton sort needed).
+constexpr int kSmallMaxN = 8192;                   // 96 KB of SoA targets in shared memory
+constexpr long long kSmallMaxPairs = 1ll << 26;
+constexpr int kSmallThreads = 512;                 // one CTA of 16 warps per SM
+
+// padded length of the staged SoA rows: a multiple of 4 candidates per lane step x 32 lanes
+__host__ __device__ __forceinline__ int small_npad(int n) { return (n + 127) & ~127; }
+
+// the target in ORIGINAL order as SoA rows x[np], y[np], z[np] (position = original index);
+// padding is NaN (its d^2 compares false: never a candidate, even for an unbounded search)
+__device__ __forceinline__ void small_stage(const IterArgs& a, float* sT) {
+    const int n = a.T.n, np = small_npad(n);
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+        float4 p = k < n ? __ldg(a.T.opts + k) : make_float4(NAN, NAN, NAN, 0.0f);
+        sT[k] = p.x;
+        sT[np + k] = p.y;
+        sT[2 * np + k] = p.z;
+    }
+    __syncthreads();
+}
+
+// nn + a3-a5 of this CTA's queries into acc (group leaders only); corr outputs when requested.
+// Lane k of a query's group of G lanes evaluates the candidate quads k, k + G, ... with packed
+// FP32 (two candidates per FADD2/FFMA2; -dx = (t + (-s_hi)) + (-s_lo), the same d^2 bits as
+// cand_d2) and keeps the u64 key minimum; the group then reduces its keys by shuffles.
+template <int METRIC>
+__device__ __forceinline__ void small_pass(const IterArgs& a, const float* sT, const Pose34& P, int glog,
+                                          float (&acc)[kSlots]) {
+    const int n = a.T.n, np = small_npad(n), nq = np >> 2;
+    const int G = 1 << glog;
+    const int sub = threadIdx.x & (G - 1);
+    const int qpb = kSmallThreads >> glog;
+    const unsigned FULL = 0xffffffffu;
+    const unsigned long long none = bound_key(a.bound2);
+    const float4* X = reinterpret_cast<const float4*>(sT);
+    const float4* Y = reinterpret_cast<const float4*>(sT + np);
+    const float4* Z = reinterpret_cast<const float4*>(sT + 2 * np);
+    // every lane of a warp runs the same number of rounds (the shuffles need the whole group)
+    const int rounds = (a.m + qpb * (int)gridDim.x - 1) / (qpb * (int)gridDim.x);
+    for (int rd = 0; rd < rounds; ++rd) {
+        const int q = (rd * (int)gridDim.x + (int)blockIdx.x) * qpb + ((int)threadIdx.x >> glog);
+        const bool on = q < a.m;
+        DF3 s;
+        unsigned long long best = none;
+        if (on) {
+            s = transform_df(P, a.src[3 * (size_t)q], a.src[3 * (size_t)q + 1], a.src[3 * (size_t)q + 2]);
+            const NegQuery nq2 = neg_query(s);
+            float bd = key_d2(best);
+#pragma unroll 2
+            for (int k = sub; k < nq; k += G) {
+                const float4 x = X[k], y = Y[k], z = Z[k];
+                const float2 d01 = pair_d2(nq2, make_float2(x.x, x.y), make_float2(y.x, y.y), make_float2(z.x, z.y));
+                const float2 d23 = pair_d2(nq2, make_float2(x.z, x.w), make_float2(y.z, y.w), make_float2(z.z, z.w));
+                if (fminf(fminf(d01.x, d01.y), fminf(d23.x, d23.y)) <= bd) {   // rare after the first few
+                    const float dd[4] = {d01.x, d01.y, d23.x, d23.y};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const unsigned long long kk = make_key(dd[c], (uint32_t)(4 * k + c));
+                        if (dd[c] <= bd && kk < best) { best = kk; bd = dd[c]; }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            if (o >= G) break;
+            const unsigned long long ot = __shfl_xor_sync(FULL, best, o);
+            best = ot < best ? ot : best;
+        }
+        if (on && sub == 0) {
+            const bool found = best != none;
+            const int j = found ? (int)key_idx(best) : -1;
+            if (a.corr_idx) a.corr_idx[q] = j;
+            if (a.corr_d2) a.corr_d2[q] = found ? key_d2(best) : INFINITY;
+            if (found) {
+                const float4 t = make_float4(sT[j], sT[np + j], sT[2 * np + j], 0.0f);
+                const float4 nrm = METRIC != CIL_POINT_TO_POINT ? __ldg(a.T.onrm + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                float d2;
+                (void)accumulate_s<METRIC>(acc, s, t, nrm, a.bound2, a.w_pp, a.w_pl, &d2);
+            }
+        }
+    }
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+icp_small_kernel(const IterArgs a, int glog) {
+    extern __shared__ float sT[];
+    __shared__ double Psh[16];
+    pdl_trigger();
+    pdl_wait();
+    if (a.run && *(volatile int*)&a.st->done) return;
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.pose_in[threadIdx.x];
+    small_stage(a, sT);
+    Pose34 P;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+    float acc[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+    small_pass<METRIC>(a, sT, P, glog, acc);
+    reduce_finalize<METRIC, true, kSmallThreads / 32>(a, acc, Psh);
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+icp_small_run_kernel(const IterArgs a, int glog, int iters) {
+    extern __shared__ float sT[];
+    __shared__ double Psh[16];
+    __shared__ double wsum[kSmallThreads / 32][kSlots];
+    __shared__ double Ssum[kSlots];
+    __shared__ double Hs[36], gsh[6], scal[2];
+    __shared__ int s_stop;
+    if (threadIdx.x < 16) Psh[threadIdx.x] = a.st->pose[threadIdx.x];
+    small_stage(a, sT);
+    const int G = (int)gridDim.x;
+    for (int it = 0; it < iters; ++it) {
+        Pose34 P;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) P.r[k] = Psh[k];
+        float acc[kSlots];
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) acc[k] = 0.0f;
+        small_pass<METRIC>(a, sT, P, glog, acc);
+        double* part = a.partials + (size_t)(it & 1) * G;      // double-buffered columns
+        cta_partial<kSmallThreads / 32>(acc, wsum, part);
+        grid_barrier(&a.st->bar_count, &a.st->bar_gen);
+        sum_partials(part, G, Ssum);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double x[6], Pn[16];
+            const int status = solve_pose_warp<METRIC>(Ssum, Psh, Hs, gsh, scal, x, Pn);
+            __syncwarp();
+            if (threadIdx.x == 0) {
+                const double sse = scal[0], cnt = scal[1];
+                bool stop = status != CIL_OK;
+                bool conv = false;
+                if (!stop) {
+                    const double th = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+                    const double tn = sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+                    conv = th < a.rot_tol && tn < a.trans_tol;
+                    stop = conv;
+                }
+                if (blockIdx.x == 0) {
+                    IcpState* st = a.st;
+                    const double rmse = cnt > 0.0 ? sqrt(sse / cnt) : 0.0;
+                    if (a.iter_log) { a.iter_log[2 * it] = cnt; a.iter_log[2 * it + 1] = rmse; }
+                    st->iters = it + 1;
+                    st->n_corr = (long long)cnt;
+                    st->rmse = rmse;
+                    st->searched += a.m;
+                    if (status != CIL_OK) {
+                        st->status = status;
+                        st->converged = 0;
+                        st->done = 1;
+                    } else {
+                        for (int i = 0; i < 16; ++i) st->pose[i] = Pn[i];
+                        if (conv) { st->converged = 1; st->done = 1; }
+                    }
+                }
+                if (status == CIL_OK)
+                    for (int i = 0; i < 16; ++i) Psh[i] = Pn[i];
+                s_stop = stop;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+}
+
 // ---------------------------------------------------------------- run bookkeeping kernels
 __global__ void run_init_kernel(IcpState* st, const double* pose_init, int* nn, uint32_t* gw, uint32_t* gp, int m,
                                 double* iter_log, int log_len) {
@@ -1566,6 +1749,85 @@ cudaError_t launch_proj(const IterArgs& a0, int metric, cudaStream_t s) {
         case CIL_POINT_TO_PLANE: return launch_proj_m<CIL_POINT_TO_PLANE>(a, s);
         case CIL_COMBINED: return launch_proj_m<CIL_COMBINED>(a, s);
         default: return launch_proj_m<CIL_POINT_TO_POINT>(a, s);
+    }
+}
+
+// ---------------------------------------------------------------- small-problem launches
+bool small_path(const cil_target* t, int64_t m) {
+    return !(debug_flags() & 64u) && m > 0 && t->v.n <= kSmallMaxN && (long long)m * t->v.n <= kSmallMaxPairs;
+}
+
+// lanes per query: the largest power of two <= 32 with m * G <= the grid's threads
+int small_glog(int64_t m) {
+    const int64_t threads = (int64_t)sm_count() * kSmallThreads;
+    int g = 0;
+    while (g < 5 && m * (int64_t)(2 << g) <= threads) ++g;
+    return g;
+}
+
+template <class K>
+cudaError_t small_attr(K kernel) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * small_npad(kSmallMaxN) * (int)sizeof(float));
+}
+
+template <int METRIC>
+cudaError_t launch_small_m(const IterArgs& a0, bool run, int iters, cudaStream_t s) {
+    static const cudaError_t e_attr = [] {
+        cudaError_t e1 = small_attr(icp_small_kernel<METRIC>);
+        cudaError_t e2 = small_attr(icp_small_run_kernel<METRIC>);
+        return e1 != cudaSuccess ? e1 : e2;
+    }();
+    if (e_attr != cudaSuccess) return e_attr;
+    IterArgs a = a0;
+    a.stamps = nullptr;
+    const int glog = small_glog(a.m);
+    const int grid = sm_count();                  // one CTA per SM (the staged target fills shared memory)
+    const size_t smem = 3 * (size_t)small_npad(a.T.n) * sizeof(float);
+    prof_begin(kProfAcc, s);
+    cudaError_t e = cudaSuccess;
+    if (run) {
+        int it = iters, gl = glog;
+        void* args[] = {(void*)&a, (void*)&gl, (void*)&it};
+        e = cudaLaunchCooperativeKernel((const void*)icp_small_run_kernel<METRIC>, dim3(grid), dim3(kSmallThreads), args,
+                                        smem, s);
+        count_launches(1);
+        if (e != cudaSuccess) {
+            // not co-schedulable: one launch per iteration (same grid and arithmetic)
+            (void)cudaGetLastError();
+            e = cudaSuccess;
+            for (int k = 0; k < iters && e == cudaSuccess; ++k) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)grid);
+                cfg.blockDim = dim3((unsigned)kSmallThreads);
+                cfg.dynamicSmemBytes = smem;
+                cfg.stream = s;
+                e = cudaLaunchKernelEx(&cfg, icp_small_kernel<METRIC>, a, glog);
+                count_launches(1);
+            }
+        }
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)kSmallThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, icp_small_kernel<METRIC>, a, glog);
+        count_launches(1);
+    }
+    prof_end(s);
+    return e;
+}
+
+cudaError_t launch_small(const IterArgs& a, int metric, bool run, int iters, cudaStream_t s) {
+    switch (metric) {
+        case CIL_POINT_TO_PLANE: return launch_small_m<CIL_POINT_TO_PLANE>(a, run, iters, s);
+        case CIL_COMBINED: return launch_small_m<CIL_COMBINED>(a, run, iters, s);
+        default: return launch_small_m<CIL_POINT_TO_POINT>(a, run, iters, s);
     }
 }
 
@@ -1757,6 +2019,13 @@ CIL_API cil_status cil_icp_iterate(const cil_target* t, const float* src, int64_
     a.run = 0;
     a.cert = 0;
     cudaStream_t s = (cudaStream_t)stream;
+    if (small_path(t, m)) {                       // brute force in one launch (caller's source order)
+        reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
+        count_launches(1);
+        cudaError_t e = launch_small(a, params->metric, false, 1, s);
+        if (e != cudaSuccess) return cuda_fail(e, "icp_small_kernel launch");
+        return CIL_OK;
+    }
     cudaError_t e = sort_source(a, src, s);
     if (e != cudaSuccess) return cuda_fail(e, "source Morton order");
     reset_ticket_kernel<<<1, 1, 0, s>>>(a.st);
@@ -1833,6 +2102,21 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
     IterArgs a;
     run_args(a, t, src, m, params, ws, iter_log);
     cudaStream_t s = (cudaStream_t)stream;
+    if (small_path(t, m)) {
+        // the whole loop in one cooperative launch, brute-force correspondences (no certificates)
+        a.cert = 0;
+        a.src = src;
+        run_init_kernel<<<1, 256, 0, s>>>(a.st, pose_init, nullptr, nullptr, nullptr, 0, iter_log, 2 * params->max_iters);
+        count_launches(1);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = launch_small(a, params->metric, true, params->max_iters, s);
+        if (e != cudaSuccess) return cuda_fail(e, "icp_small_run_kernel launch");
+        run_final_kernel<<<1, 32, 0, s>>>(a.st, res);
+        count_launches(1);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
+        return CIL_OK;
+    }
     rc = run_begin(a, src, m, pose_init, params->max_iters, s);
     if (rc != CIL_OK) return rc;
     for (int it = 0; it < params->max_iters; ++it) {

@@ -29,16 +29,20 @@ def test_iterate_c4_full(cil, frac):
     check_iteration(cil, w, _perturb(w.gt_pose, frac), "point_to_plane")
 
 
-def test_run_c4_full_bench_configuration(cil):
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+def test_run_c4_full_bench_configuration(cil, metric):
     """the bench's run (50 iterations, certified warm start) against the oracle's 50 full
-    iterations, and bit for bit against 50 chained stateless GPU iterations"""
-    w = W.c4("point_to_plane")
-    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
-    prm = cil.make_params("point_to_plane", w.max_iters, w.max_dist)
+    iterations, and bit for bit against 50 chained stateless GPU iterations -- for both C4
+    variants (BASELINE.json configs[3] "point-to-point and point-to-plane variants"; the
+    point-to-point run has the slowest certificate dynamics)"""
+    w = W.c4(metric)
+    nrm = dev(w.target_normals) if metric == "point_to_plane" else None
+    t = cil.cil_target_build(dev(w.target), nrm)
+    prm = cil.make_params(metric, w.max_iters, w.max_dist)
     res_t, log = cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)
     res = cil.decode_result(res_t)
-    o = oracle.icp_run(None, w.target_normals, w.source, "point_to_plane", w.max_iters, w.max_dist,
-                       tree=W.oracle_tree(w))
+    o = oracle.icp_run(None, w.target_normals if metric == "point_to_plane" else None, w.source, metric,
+                       w.max_iters, w.max_dist, tree=W.oracle_tree(w))
     assert res.status == o.status == 0 and res.iterations == o.iterations == w.max_iters
     dr = W.rot_angle(res.pose[:3, :3] @ o.pose[:3, :3].T)
     dt = np.abs(res.pose[:3, 3] - o.pose[:3, 3]).max()
@@ -49,6 +53,12 @@ def test_run_c4_full_bench_configuration(cil):
     for _ in range(w.max_iters):
         P, *_ = cil.cil_icp_iterate(t, src, P, prm, want_sys=False)
     assert np.array_equal(P.cpu().numpy(), res.pose)
+
+
+@pytest.mark.parametrize("frac", [0.0, 1.0])
+def test_iterate_c4_point_to_point_full(cil, frac):
+    w = W.c4("point_to_point")
+    check_iteration(cil, w, _perturb(w.gt_pose, frac), "point_to_point")
 
 
 def test_iterate_c5_2e22_every_query(cil):

@@ -312,6 +312,60 @@ def test_run_c1(cil):
 
 
 @pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point", "combined"])
+def test_small_path_equals_tree_path(cil, metric):
+    """C1 (4,096 points) takes the small-problem path (brute-force exact NN staged in shared
+    memory, one cooperative launch for the run); with it disabled (debug bit 6) the BVH
+    engine runs.  Both must return the same exact correspondences (bit-equal, no near ties
+    here) and systems equal up to the summation order; run poses within 1e-9."""
+    w = W.c1()
+    prm = _params(cil, metric, w.max_iters, w.max_dist)
+    prm1 = _params(cil, metric, 1, w.max_dist)
+    out = []
+    try:
+        for flags in (0, 64):
+            cil.set_debug_flags(flags)
+            t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+            P = dev(_perturb(w.gt_pose, 0.3))
+            pose_out, sys_t, ci, cd = cil.cil_icp_iterate(t, dev(w.source), P, prm1, want_corr=True)
+            res_t, log = cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)
+            out.append((ci.cpu().numpy(), cd.cpu().numpy(), cil.decode_system(sys_t), cil.decode_result(res_t),
+                        log.cpu().numpy()))
+    finally:
+        cil.set_debug_flags(0)
+    (ia, da, sa, ra, la), (ib, db, sb, rb, lb) = out
+    assert np.array_equal(ia, ib) and np.array_equal(da, db)
+    # (fp32 per-thread sums grouped differently: ~1e-8 relative, SURVEY.md A.1)
+    assert sa.n_corr == sb.n_corr and np.linalg.norm(sa.H - sb.H) <= 1e-6 * np.linalg.norm(sb.H)
+    assert np.linalg.norm(sa.g - sb.g) <= 1e-5 * max(np.linalg.norm(sb.g), 1e-12)
+    assert ra.status == rb.status == 0 and ra.iterations == rb.iterations
+    assert W.rot_angle(ra.pose[:3, :3] @ rb.pose[:3, :3].T) <= 1e-6 and np.abs(ra.pose[:3, 3] - rb.pose[:3, 3]).max() <= 1e-7
+    np.testing.assert_array_equal(la[:, 0], lb[:, 0])
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (7, 100), (300, 37), (8192, 8000), (2000, 33000)])
+def test_small_path_ragged(cil, n, m):
+    """ragged small problems (one target point, more/less sources than targets, a group size
+    of 1..32 lanes per query, the largest staged target) against the oracle's iteration"""
+    rng = np.random.default_rng(n * 7 + m)
+    T = rng.standard_normal((n, 3)).astype(np.float32)
+    N = rng.standard_normal((n, 3))
+    N = (N / np.linalg.norm(N, axis=1, keepdims=True)).astype(np.float32)
+    S = (T[rng.integers(0, n, m)] + rng.normal(0, 0.05, (m, 3))).astype(np.float32)
+    t = cil.cil_target_build(dev(T), dev(N))
+    prm = cil.make_params("point_to_plane", 1, 0.2)
+    pose_out, sys_t, ci, cd = cil.cil_icp_iterate(t, dev(S), dev(np.eye(4)), prm, want_corr=True)
+    o = oracle.icp_system(T, N, S, np.eye(4), "point_to_plane", 0.2)
+    o_idx = np.stack([o.corr_idx, np.where(np.isfinite(o.corr_d2nd), 0, -1)], 1)
+    o_d2 = np.stack([o.corr_d2, o.corr_d2nd], 1)
+    check_nn(T, S.astype(np.float64), ci.cpu().numpy(), cd.cpu().numpy(), o_idx, o_d2, max_d2=0.04)
+    gs = cil.decode_system(sys_t)
+    r = oracle.icp_system_from_corr(T, N, S, np.eye(4), "point_to_plane", ci.cpu().numpy().astype(np.int32))
+    assert r.count == gs.n_corr
+    if r.count:
+        assert np.linalg.norm(gs.H - r.H) <= 1e-6 * np.linalg.norm(r.H)
+
+
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point", "combined"])
 def test_run_c4_reduced(cil, metric):
     check_run(cil, W.c4("point_to_plane" if metric == "combined" else metric, rings=16, az=8000), metric)
 

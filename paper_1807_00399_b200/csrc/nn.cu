@@ -42,10 +42,10 @@ struct NNQueries {
 };
 
 // counting sort of the queries by coarse cell: count, (scan), scatter
-__global__ void qcell_count_kernel(TargetView T, const float* __restrict__ q, int m, uint32_t* __restrict__ qcell,
-                                   uint32_t* __restrict__ cnt) {
+__global__ void qcell_count_kernel(TargetView T, const float* __restrict__ q, int m, int qbits,
+                                   uint32_t* __restrict__ qcell, uint32_t* __restrict__ cnt) {
     const float4 Q = __ldg(T.quant);
-    const int shift = 3 * kMortonBits - T.coarse_bits;
+    const int shift = 3 * kMortonBits - qbits;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const uint32_t c = (uint32_t)(morton_of(Q, q[3 * (size_t)i], q[3 * (size_t)i + 1], q[3 * (size_t)i + 2]) >> shift);
         qcell[i] = c;
@@ -116,7 +116,10 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
     if (!idx && !sqdist) return CIL_OK;
     cudaStream_t s = (cudaStream_t)stream;
     // stream-ordered scratch: work counter | cell counts | qcell | perm | scan temp
-    const int64_t ncell = 1ll << t->v.coarse_bits;
+    // query order: counting sort by coarse Morton cell (the grid search only needs packets of
+    // neighbours: at most 2^18 cells, a cheaper scan)
+    const int qbits = t->v.gpts ? std::min(t->v.coarse_bits, 18) : t->v.coarse_bits;
+    const int64_t ncell = 1ll << qbits;
     const size_t b_cnt = align_up((size_t)(ncell + 1) * 4, 256);
     const size_t b_q = align_up((size_t)m * 4, 256);
     const size_t b_scan = scan_temp_bytes(ncell + 1);
@@ -134,7 +137,7 @@ CIL_API cil_status cil_nn_query(const cil_target* t, const float* queries, int64
                  INFINITY, idx, sqdist};
     if (e == cudaSuccess) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8));
-        qcell_count_kernel<<<g, 256, 0, s>>>(t->v, queries, (int)m, qcell, cnt);
+        qcell_count_kernel<<<g, 256, 0, s>>>(t->v, queries, (int)m, qbits, qcell, cnt);
         const int nscan = scan_exclusive_u32(cnt, ncell + 1, scan_tmp, s);
         qcell_scatter_kernel<<<g, 256, 0, s>>>(qcell, (int)m, cnt, perm);
         count_launches(2 + nscan);

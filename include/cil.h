@@ -216,7 +216,9 @@ cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const d
    n . (view - p) >= 0.  k in [3, 16].  view: HOST double[3] (NULL = the origin).
    normals: device fp32 [n*3] in the target's original order; curvature (nullable): device
    fp32 [n] = lambda_min / trace.  The result can be passed to cil_target_build as the
-   normals of a new target (the index itself is immutable). */
+   normals of a new target (the index itself is immutable).  Coordinates are expected to be
+   finite; a point whose k-neighbourhood holds fewer than 3 finite neighbours (a non-finite
+   point, or k-NN sets emptied by non-finite targets) gets a zero normal and curvature 0. */
 cil_status cil_estimate_normals(const cil_target* t, int32_t k, const double* view, float* normals,
                                 float* curvature, cil_stream_t stream);
 

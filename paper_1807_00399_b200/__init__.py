@@ -262,25 +262,47 @@ def make_params(metric: str | int = "point_to_plane", max_iters: int = 1, max_co
 class Target:
     """Owning handle of a cil_target (built on the GPU, immutable)."""
 
-    def __init__(self, handle: int, n: int, keep=()):
+    def __init__(self, handle: int, n: int, keep=(), stream=None):
         self.handle = handle
         self.n = n
         self._keep = keep
+        self._streams = {}
+        self.use(stream)                      # the build stream
 
     def info(self) -> cil_target_info:
         inf = cil_target_info()
         _check(_lib.cil_target_get_info(self.handle, C.byref(inf)), "cil_target_get_info")
         return inf
 
+    def use(self, stream=None) -> int:
+        """the stream pointer of a call on this target; remembers the stream, so that free()
+        orders the release after the work of every stream the target was used on"""
+        st = torch.cuda.current_stream() if stream is None else stream
+        self._streams[st.cuda_stream] = st
+        return st.cuda_stream
+
+    def _release(self, stream) -> int:
+        st = torch.cuda.current_stream() if stream is None else stream
+        for ptr, other in self._streams.items():
+            if ptr != st.cuda_stream:
+                ev = torch.cuda.Event()
+                ev.record(other)
+                st.wait_event(ev)
+        self._streams = {}
+        return st.cuda_stream
+
     def free(self, stream=None) -> None:
+        """stream-ordered release on `stream` (default: the current stream), after the work
+        already enqueued on every stream this target was used on.  Free targets explicitly;
+        garbage collection does the same from whatever stream is current then."""
         if self.handle:
-            _check(_lib.cil_target_free(self.handle, _stream_ptr(stream)), "cil_target_free")
+            _check(_lib.cil_target_free(self.handle, self._release(stream)), "cil_target_free")
             self.handle = None
 
     def __del__(self):
         try:
             if self.handle and torch.cuda.is_available():
-                _lib.cil_target_free(self.handle, None)
+                _lib.cil_target_free(self.handle, self._release(None))
         except Exception:
             pass
 
@@ -299,7 +321,7 @@ def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, lea
     h = _vp()
     _check(_lib.cil_target_build(_ptr(pts), _ptr(normals), pts.shape[0], C.byref(prm), _stream_ptr(stream),
                                  C.byref(h)), "cil_target_build")
-    return Target(h.value, pts.shape[0])
+    return Target(h.value, pts.shape[0], stream=stream)
 
 
 def cil_target_free(t: Target, stream=None) -> None:
@@ -316,7 +338,7 @@ def cil_nn_query(t: Target, queries: torch.Tensor, max_dist: float = math.inf, s
     if sqdist is None:
         sqdist = torch.empty(m, dtype=torch.float32, device=dev)
     _check(_lib.cil_nn_query(t.handle, _ptr(queries), m, float(max_dist), _ptr(idx), _ptr(sqdist),
-                             _stream_ptr(stream)), "cil_nn_query")
+                             t.use(stream)), "cil_nn_query")
     return idx, sqdist
 
 
@@ -327,7 +349,7 @@ def cil_estimate_normals(t: Target, k: int = 10, view=(0.0, 0.0, 0.0), stream=No
     nrm = torch.empty((t.n, 3), dtype=torch.float32, device=device)
     cur = torch.empty(t.n, dtype=torch.float32, device=device) if want_curvature else None
     v = (C.c_double * 3)(*[float(x) for x in view])
-    _check(_lib.cil_estimate_normals(t.handle, int(k), C.byref(v), _ptr(nrm), _ptr(cur), _stream_ptr(stream)),
+    _check(_lib.cil_estimate_normals(t.handle, int(k), C.byref(v), _ptr(nrm), _ptr(cur), t.use(stream)),
            "cil_estimate_normals")
     return nrm, cur
 
@@ -367,7 +389,7 @@ def cil_icp_iterate(t: Target, src: torch.Tensor, pose_in: torch.Tensor, params:
     ci = torch.empty(m, dtype=torch.int32, device=dev) if want_corr else None
     cd = torch.empty(m, dtype=torch.float32, device=dev) if want_corr else None
     _check(_lib.cil_icp_iterate(t.handle, _ptr(src), m, _ptr(pose_in), C.byref(params), _ptr(ws), ws.numel(),
-                                _ptr(pose_out), _ptr(sys_t), _ptr(ci), _ptr(cd), _stream_ptr(stream)),
+                                _ptr(pose_out), _ptr(sys_t), _ptr(ci), _ptr(cd), t.use(stream)),
            "cil_icp_iterate")
     return pose_out, sys_t, ci, cd
 
@@ -386,7 +408,7 @@ def cil_icp_run(t: Target, src: torch.Tensor, pose_init: torch.Tensor, params: c
     if iter_log is None and want_log:
         iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev)
     _check(_lib.cil_icp_run(t.handle, _ptr(src), m, _ptr(pose_init), C.byref(params), _ptr(ws), ws.numel(),
-                            _ptr(res), _ptr(iter_log), _stream_ptr(stream)), "cil_icp_run")
+                            _ptr(res), _ptr(iter_log), t.use(stream)), "cil_icp_run")
     return res, iter_log
 
 
@@ -464,13 +486,13 @@ class ShardRun:
         self.sums = torch.zeros(32, dtype=torch.float64, device=dev)
         self.iter_log = torch.empty((params.max_iters, 2), dtype=torch.float64, device=dev) if want_log else None
         _check(_lib.cil_icp_shard_begin(t.handle, _ptr(src_shard), self.m, _ptr(pose_init), C.byref(params),
-                                        _ptr(self.ws), self.ws.numel(), _ptr(self.iter_log), _stream_ptr(stream)),
+                                        _ptr(self.ws), self.ws.numel(), _ptr(self.iter_log), t.use(stream)),
                "cil_icp_shard_begin")
 
     def accumulate(self) -> torch.Tensor:
         _check(_lib.cil_icp_shard_accumulate(self.t.handle, _ptr(self.src), self.m, C.byref(self.params),
                                              _ptr(self.ws), self.ws.numel(), _ptr(self.sums),
-                                             _stream_ptr(self.stream)), "cil_icp_shard_accumulate")
+                                             self.t.use(self.stream)), "cil_icp_shard_accumulate")
         return self.sums
 
     def finish(self, reduced: torch.Tensor | None = None) -> None:
@@ -489,13 +511,19 @@ def icp_run_distributed(t: Target, src_shard: torch.Tensor, pose_init: torch.Ten
                         group=None, stream=None):
     """cil_icp_run over a source split across the ranks of torch.distributed `group`: one
     all-reduce of 32 fp64 sums per iteration (NCCL on GPUs).  Every rank gets the same pose."""
+    import contextlib
     import torch.distributed as dist
-    run = ShardRun(t, src_shard, pose_init, params, stream=stream)
-    for _ in range(params.max_iters):
-        s = run.accumulate()
-        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
-        run.finish()
-    return run.result(), run.iter_log
+    # every step runs on ONE stream, made current for the duration: the library calls use the
+    # current stream and NCCL orders the all-reduce against the current stream (a non-current
+    # `stream` would let the reduce read the sums before the accumulation wrote them)
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        run = ShardRun(t, src_shard, pose_init, params)
+        for _ in range(params.max_iters):
+            s = run.accumulate()
+            dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+            run.finish()
+        return run.result(), run.iter_log
 
 
 # ---------------------------------------------------------------- voxel-grid downsampling (NEXT-4)

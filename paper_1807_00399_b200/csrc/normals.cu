@@ -198,8 +198,19 @@ knn_normals_kernel(TargetView T, int k, double vx, double vy, double vz, float* 
         }
         if (v == 0) break;
     }
-    // 2. mean and 1/k covariance (fp64) of the k neighbours
-    const int kk = min(k, T.n);
+    // 2. mean and 1/k covariance (fp64) of the k neighbours actually found (a non-finite query
+    //    or target coordinate leaves slots at the "nothing" key: fewer than 3 -> zero normal)
+    int kk = 0;
+#pragma unroll
+    for (int c = 0; c < kKmax; ++c)
+        kk += (c < min(k, T.n) && key_idx(top[c]) != 0xffffffffu && (uint32_t)(top[c] >> 32) <= 0x7f800000u) ? 1 : 0;
+    if (kk < 3) {
+        normals[3 * (size_t)qid] = 0.0f;
+        normals[3 * (size_t)qid + 1] = 0.0f;
+        normals[3 * (size_t)qid + 2] = 0.0f;
+        if (curvature) curvature[qid] = 0.0f;
+        return;
+    }
     double mu[3] = {0.0, 0.0, 0.0};
     float4 P[kKmax];
 #pragma unroll

@@ -498,3 +498,17 @@ def test_run_empty_source(cil):
     empty = torch.empty((0, 3), dtype=torch.float32, device="cuda")
     res = cil.decode_result(cil.cil_icp_run(t, empty, dev(np.eye(4)), cil.make_params("point_to_plane", 5, 0.1))[0])
     assert res.status == cil.CIL_NO_CORRESPONDENCES and res.iterations == 1 and np.array_equal(res.pose, np.eye(4))
+
+
+def test_normals_non_finite_point(cil):
+    """a NaN target point must not fault the normal kernel: it gets a zero normal, the others
+    are unit vectors (cil.h: fewer than 3 finite neighbours -> zero normal)"""
+    rng = np.random.default_rng(5)
+    P = np.stack([rng.random(3000), rng.random(3000), np.zeros(3000)], 1).astype(np.float32)
+    P[17] = np.nan
+    t = cil.cil_target_build(dev(P), None)
+    n, c = cil.cil_estimate_normals(t, 10, (0.0, 0.0, 1.0))
+    n = n.cpu().numpy()
+    assert np.array_equal(n[17], np.zeros(3, np.float32))
+    ok = np.ones(3000, bool); ok[17] = False
+    assert np.allclose(np.linalg.norm(n[ok], axis=1), 1.0, atol=1e-5)

@@ -82,3 +82,56 @@ def test_shard_stop_rules(cil):
     full = cil.decode_result(cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm)[0])
     assert a.converged and b.converged and a.iterations == b.iterations == full.iterations < 50
     assert np.array_equal(a.pose, b.pose)
+
+
+def test_distributed_driver_on_a_side_stream(cil):
+    """icp_run_distributed through a real process group (NCCL, world size 1) with a stream that
+    is NOT the current one: the driver makes it current for every step, so the all-reduce is
+    ordered after the accumulation that writes the sums; the pose equals the unsplit run's
+    (same shard = the whole source, the same reduction order)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    w = W.c4("point_to_plane", rings=16, az=8000)
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    src = dev(w.source)
+    prm = cil.make_params("point_to_plane", 12, w.max_dist)
+    res_t, _ = cil.cil_icp_run(t, src, dev(np.eye(4)), prm)
+    ref = cil.decode_result(res_t)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        side = torch.cuda.Stream()
+        P0 = dev(np.eye(4))
+        side.wait_stream(torch.cuda.current_stream())
+        res_d, _ = cil.icp_run_distributed(t, src, P0, prm, stream=side)
+        torch.cuda.synchronize()
+        got = cil.decode_result(res_d)
+    finally:
+        dist.destroy_process_group()
+    assert got.status == ref.status == 0 and got.iterations == ref.iterations
+    assert np.abs(got.pose - ref.pose).max() <= 1e-9
+
+
+def test_target_freed_on_another_stream(cil):
+    """a target used on a side stream and freed from the default stream: the release waits for
+    the side stream's queries (the results stay correct after the free)"""
+    rng = np.random.default_rng(3)
+    T = rng.random((200_000, 3)).astype(np.float32)
+    Q = rng.random((300_000, 3)).astype(np.float32)
+    side = torch.cuda.Stream()
+    dT, dQ = dev(T), dev(Q)
+    side.wait_stream(torch.cuda.current_stream())
+    t = cil.cil_target_build(dT, None)
+    with torch.cuda.stream(side):
+        gi, gd = cil.cil_nn_query(t, dQ)
+    t.free()                                   # from the current (default) stream
+    junk = torch.empty(64 << 20, dtype=torch.uint8, device="cuda").fill_(7)   # reuse freed memory
+    torch.cuda.synchronize()
+    from scipy.spatial import cKDTree
+    d, i = cKDTree(T.astype(np.float64)).query(Q.astype(np.float64), k=1)
+    assert (gi.cpu().numpy() == i).mean() > 0.9999
+    del junk

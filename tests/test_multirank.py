@@ -103,20 +103,16 @@ def test_split_problem_allreduce_gloo_world2():
 
 def _driver_worker(rank, world, port, out):
     """icp_run_distributed's control flow with the shard steps stubbed by the oracle (no GPU):
-    one SUM all-reduce of the 32 sums per iteration, the same pose on every rank"""
+    one SUM all-reduce of the 32 sums per iteration, the same pose on every rank.  The package
+    is imported as is (loading libcil.so needs no GPU) and its ShardRun is replaced by a stub
+    that computes the shard's normal equations with the oracle."""
     import numpy as np
     import oracle
+    import paper_1807_00399_b200 as cil
     from tests import workloads as W
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # the driver's source, executed with its shard steps replaced (the package itself loads
-        # libcil.so, which needs no GPU to load, but its kernels do)
-        src = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                "paper_1807_00399_b200", "__init__.py")).read()
-        start = src.index("def icp_run_distributed(")
-        end = src.index("\n\n\n", start)
-        ns = {"torch": torch, "Target": object, "cil_icp_params": object}
         w = W.c1()
         half = w.m // 2
         sl = slice(0, half) if rank == 0 else slice(half, w.m)
@@ -141,12 +137,11 @@ def _driver_worker(rank, world, port, out):
             def result(self):
                 return self.P
 
-        ns["ShardRun"] = FakeRun
-        exec(src[start:end], ns)
+        cil.ShardRun = FakeRun
 
         class Prm:
             max_iters = 3
-        P, _ = ns["icp_run_distributed"](None, None, None, Prm)
+        P, _ = cil.icp_run_distributed(None, None, None, Prm)
         out[rank] = P.tolist()
     finally:
         dist.destroy_process_group()

@@ -218,6 +218,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     cil.profile_enable(False)
     prof = cil.profile_read()
+    prof_iters = None
+    if not args.split and not args.no_iter_profile:
+        t_p = cil.cil_target_build(tgt, nrm, args.leaf)
+        prof_iters = _iteration_profile(cil, t_p, src, w, metric, iters, flush, dev)
+        t_p.free()
     tot_max, total_pairs = reduce_over_ranks(tot_ms, float(m_rank) * iters * args.steps, world, dev)
     r = cil.decode_result(res)
     # e2e: the public host-buffer API on every rank (pinned host inputs, H2D inside the timed
@@ -237,7 +242,7 @@ def run_ours(args, rank, world, local_rank):
     bpp = _bytes_per_pair(metric)
     achieved = bpp * m_rank / (it_ms * 1e-3) / 1e9
     peak, peak_src = _peak_hbm()
-    traffic = _traffic_from_profiles(args.workload)
+    traffic = _traffic_from_profiles(args.workload, args.leaf or 16)
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -265,7 +270,8 @@ def run_ours(args, rank, world, local_rank):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_pair": bpp, "peak_source": peak_src,
                      "frac_of_8TBps_nominal": achieved / 8000.0},
-        "roofline_issue": _issue_roofline_from_profiles(),
+        "roofline_issue": _issue_roofline_from_profiles(args.leaf or 16),
+        "iterations_profile": prof_iters,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -280,26 +286,38 @@ def C_sizeof(ct):
     return ctypes.sizeof(ct)
 
 
-def _traffic_from_profiles(workload):
+def _traffic_from_profiles(workload, leaf):
     """dram bytes of one steady-state ICP iteration (select + nn + acc kernels) from the committed
-    ncu --set full captures (profiles/traffic.json)"""
+    ncu --set full captures (profiles/traffic.json) -- only if they were taken with the leaf size
+    the bench times (else None: the counters would describe another kernel build)"""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             t = json.load(f).get(workload)
-        return None if t is None else t.get("steady_iteration_bytes")
+        if t is None or int(t.get("leaf_size", -1)) != leaf:
+            return None
+        return t.get("steady_iteration_bytes")
     except Exception:
         return None
 
 
-def _issue_roofline_from_profiles():
+NCU_FULL_SEARCH = "profiles/r2_ncu_nn_it3_c4cert.txt"
+
+
+def _issue_roofline_from_profiles(leaf):
     """the search kernel's instruction-issue roofline on a full-search iteration, from the
-    committed ncu --set full capture (profiles/r1_ncu_nn_it3_c4cert.txt): executed
-    warp-instructions / duration against 148 SMs x 4 schedulers x sm_max_mhz"""
-    p = os.path.join(ROOT, "profiles", "r1_ncu_nn_it3_c4cert.txt")
+    committed ncu --set full capture: executed warp-instructions / duration against 148 SMs x 4
+    schedulers x sm_max_mhz.  Refused (None) unless the capture's kernel template is the timed
+    leaf size (icp_nn_kernel<leaf, 1>)."""
+    import re
+    p = os.path.join(ROOT, NCU_FULL_SEARCH)
     try:
         vals = {}
-        for line in open(p):
+        lines = open(p).read().splitlines()
+        m = re.search(r"icp_nn_kernel<(\d+),", lines[0])
+        if not m or int(m.group(1)) != leaf:
+            return None
+        for line in lines:
             parts = line.split()
             if line.strip().startswith("Duration"):
                 vals["us"] = float(parts[1]) * (1e-3 if parts[2] == "ns" else 1.0)
@@ -314,11 +332,53 @@ def _issue_roofline_from_profiles():
             pass
         ach = vals["inst"] / (vals["us"] * 1e-6)
         peak = 148 * 4 * mhz * 1e6
-        return {"bound": "issue", "kernel": "icp_nn_kernel, full-search iteration (ncu --set full capture)",
+        return {"bound": "issue", "kernel": f"icp_nn_kernel<{leaf}, 1>, full-search iteration 3 (ncu --set full capture)",
                 "achieved": ach, "peak": peak, "unit": "warp-instructions/s", "frac": ach / peak,
-                "ncu_issue_slots_busy": vals.get("busy"), "source": "profiles/r1_ncu_nn_it3_c4cert.txt"}
+                "ncu_issue_slots_busy": vals.get("busy"), "source": NCU_FULL_SEARCH}
     except Exception:
         return None
+
+
+def _iteration_profile(cil, t, src, w, metric, iters, flush, dev):
+    """SURVEY.md 8(d)'s three C4 numbers, device-timed with CUDA events (median of 5, L2 flushed
+    before each): (i) a cold full-search iteration at the identity (stateless cil_icp_iterate);
+    (ii) the steady certified iteration = (run(iters) - run(iters - 20)) / 20, i.e. the mean of
+    the last 20 iterations of the certified run; (iii) the run average (= the headline)."""
+    import torch
+    P0 = torch.eye(4, dtype=torch.float64, device=dev)
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    p1 = cil.make_params(metric, 1, w.max_dist)
+    ws = cil.alloc_workspace(w.m, cil.make_params(metric, iters, w.max_dist), dev)
+    cold = timed(lambda: cil.cil_icp_iterate(t, src, P0, p1, ws=ws, want_sys=False))
+    runs = {}
+    for k in (iters, max(iters - 20, 1)):
+        pk = cil.make_params(metric, k, w.max_dist)
+        runs[k] = timed(lambda: cil.cil_icp_run(t, src, P0, pk, ws=ws, want_log=False))
+    k0 = max(iters - 20, 1)
+    steady = (runs[iters] - runs[k0]) / max(iters - k0, 1)
+    bpp = _bytes_per_pair(metric)
+    peak, _ = _peak_hbm()
+    out = {}
+    for name, ms in (("i_cold_full_search_iterate", cold), ("ii_steady_certified_iteration", steady),
+                     ("iii_run_average_iteration", runs[iters] / iters)):
+        out[name] = {"ms": ms, "pairs_per_s": w.m / (ms * 1e-3), "hbm_frac": bpp * w.m / (ms * 1e-3) / 1e9 / peak}
+    out["_how"] = ("(i) stateless cil_icp_iterate at the identity, L2 flushed; (ii) (run(%d) - run(%d)) / %d; "
+                   "(iii) run(%d) / %d; target prebuilt, median of 5" % (iters, k0, iters - k0, iters, iters))
+    return out
 
 
 def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
@@ -388,30 +448,75 @@ def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
 
 
 # ---------------------------------------------------------------------------- oracle arm
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def _oracle_sample(w, metric, sample_pts, iters, threads):
-    """the oracle as it stands: kd-tree over the full target, ICP on a seeded subset of the
-    source (same pose sequence semantics: identity init, fixed iterations)"""
+    """the oracle as it stands: kd-tree over the full target (timed apart), ICP on a seeded
+    subset of the source (identity init, fixed iterations); threads = 0: all host cores"""
     import oracle
-    if threads:
-        oracle.set_threads(threads)
-    rng = np.random.default_rng(7)
-    sel = np.sort(rng.choice(w.m, size=min(sample_pts, w.m), replace=False))
-    src = np.ascontiguousarray(w.source[sel])
-    t0 = time.perf_counter()
-    tree = oracle.KDTree(w.target)
-    t1 = time.perf_counter()
-    res = oracle.icp_run(None, w.target_normals, src, metric, iters, w.max_dist, tree=tree)
-    t2 = time.perf_counter()
-    return {"value": len(sel) * iters / (t2 - t0), "build_s": t1 - t0, "icp_s": t2 - t1, "pairs": len(sel) * iters,
-            "cores": oracle.get_threads(), "status": res.status}
+    all_cores = oracle.get_threads()
+    oracle.set_threads(threads or all_cores)
+    try:
+        rng = np.random.default_rng(7)
+        sel = np.sort(rng.choice(w.m, size=min(sample_pts, w.m), replace=False))
+        src = np.ascontiguousarray(w.source[sel])
+        t0 = time.perf_counter()
+        tree = oracle.KDTree(w.target)
+        t1 = time.perf_counter()
+        res = oracle.icp_run(None, w.target_normals if metric != "point_to_point" else None, src, metric, iters,
+                             w.max_dist, tree=tree)
+        t2 = time.perf_counter()
+        return {"build_s": t1 - t0, "icp_s": t2 - t1, "sample": len(sel), "pairs": len(sel) * iters,
+                "cores": oracle.get_threads(), "status": res.status, "tree": tree}
+    finally:
+        oracle.set_threads(all_cores)
+
+
+def _amortised_rate(r, w):
+    """pairs/s of the sample with the index build charged in proportion to the sample's share of
+    the full step (the GPU step builds once per m_full x iterations pairs)"""
+    return r["pairs"] / (r["icp_s"] + r["build_s"] * r["sample"] / w.m)
 
 
 def _cpu_baseline(w, metric, args):
+    """the oracle on the host cores -- all cores and 1 thread, median of 3, kd-tree
+    build reported apart, plus one full-source iteration at the identity (all cores)"""
+    import oracle
     iters = args.iters or w.max_iters
-    r = _oracle_sample(w, metric, args.cpu_sample, iters, 0)
-    return {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
-            "sample": f"{r['pairs'] // iters} of {w.m} source points (seeded subset) x {iters} iterations against "
-                      f"the full {w.n}-point target, incl. kd-tree build ({r['build_s']:.2f} s + icp {r['icp_s']:.2f} s)"}
+    med = lambda rs, k: float(np.median([r[k] for r in rs]))
+    allc = [_oracle_sample(w, metric, args.cpu_sample, iters, 0) for _ in range(3)]
+    one = [_oracle_sample(w, metric, args.cpu_sample_1t, iters, 1) for _ in range(3)]
+    tree = allc[-1]["tree"]
+    full = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle.icp_system(None, w.target_normals if metric != "point_to_point" else None, w.source, np.eye(4), metric,
+                          w.max_dist, tree=tree, want_corr=False)
+        full.append(time.perf_counter() - t0)
+    rate_all = float(np.median([_amortised_rate(r, w) for r in allc]))
+    rate_one = float(np.median([_amortised_rate(r, w) for r in one]))
+    return {"value": rate_all, "unit": UNIT, "cores": allc[0]["cores"], "kind": "oracle",
+            "cpu_model": _cpu_model(),
+            "sample": (f"{args.cpu_sample} of {w.m} source points (seeded subset) x {iters} iterations against the full "
+                       f"{w.n}-point target, median of 3; the kd-tree build is timed apart and charged in proportion "
+                       f"to the sample's share of a full step"),
+            "all_cores": {"cores": allc[0]["cores"], "pairs_per_s": rate_all,
+                          "pairs_per_s_icp_only": float(np.median([r["pairs"] / r["icp_s"] for r in allc])),
+                          "kd_build_s": med(allc, "build_s"), "icp_s": med(allc, "icp_s")},
+            "one_thread": {"cores": 1, "sample_points": args.cpu_sample_1t, "pairs_per_s": rate_one,
+                           "pairs_per_s_icp_only": float(np.median([r["pairs"] / r["icp_s"] for r in one])),
+                           "kd_build_s": med(one, "build_s"), "icp_s": med(one, "icp_s")},
+            "full_source_iteration_at_identity": {"cores": allc[0]["cores"], "s": float(np.median(full)),
+                                                  "pairs_per_s": w.m / float(np.median(full))}}
 
 
 def run_reference(args, rank, world):
@@ -423,21 +528,23 @@ def run_reference(args, rank, world):
     for _ in range(args.warmup):
         _oracle_sample(w, w.metric, max(1024, args.cpu_sample // 16), 1, 0)
     tot = 0.0
-    pairs = 0
+    rates = []
     for _ in range(args.steps):
         r = _oracle_sample(w, w.metric, args.cpu_sample, iters, 0)
-        tot += r["build_s"] + r["icp_s"]
-        pairs += r["pairs"]
-    value = pairs / tot
+        step = r["icp_s"] + r["build_s"] * r["sample"] / w.m
+        tot += step
+        rates.append(r["pairs"] / step)
+    value = float(np.sum([r for r in rates]) / len(rates))
     sample = (f"{args.cpu_sample} of {w.m} source points (seeded subset) x {iters} iterations against the full "
-              f"{w.n}-point target per step, incl. kd-tree build")
+              f"{w.n}-point target per step; the kd-tree build (timed every step) is charged in proportion to the "
+              f"sample's share of the full step, as the GPU step builds once per {w.m} x {iters} pairs")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{w.name}: BASELINE.json configs[3], {w.metric}, {iters} iterations, "
                                    f"max dist {w.max_dist} m", "n_target": w.n, "n_source": w.m},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": _cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -451,8 +558,10 @@ def main():
     ap.add_argument("--iters", type=int, default=0, help="override the config's iteration count")
     ap.add_argument("--leaf", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--cpu-sample-1t", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-iter-profile", action="store_true")
     ap.add_argument("--split", action="store_true",
                     help="one frame pair split across the ranks (SURVEY.md 8(e): NCCL all-reduce of the 32 "
                          "fp64 sums per iteration, strong scaling) instead of one frame pair per rank")

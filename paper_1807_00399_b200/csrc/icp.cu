@@ -337,9 +337,29 @@ __device__ __forceinline__ int solve_pose_warp(const double* S, const double* P,
     return status;
 }
 
+// What a6 + a7 write, by value: passing the whole kernel-parameter IterArgs by reference into a
+// noinline function made every thread of the accumulation kernels copy it (~430 B) to local
+// memory at kernel entry (32 MB of local stores per C4 iteration).
+struct FinArgs {
+    IcpState* st;
+    double* iter_log;
+    double* pose_out;
+    cil_icp_system* sys;
+    unsigned long long* stamps;
+    double rot_tol, trans_tol;
+    int run;
+};
+
+__device__ __forceinline__ FinArgs fin_args(const IterArgs& a) {
+    FinArgs f;
+    f.st = a.st; f.iter_log = a.iter_log; f.pose_out = a.pose_out; f.sys = a.sys; f.stamps = a.stamps;
+    f.rot_tol = a.rot_tol; f.trans_tol = a.trans_tol; f.run = a.run;
+    return f;
+}
+
 // finalize with the warp solve (warp 0 of the last CTA; the projective engine)
 template <int METRIC>
-__device__ __noinline__ void finalize_warp(const IterArgs& a, const double* S, const double* P) {
+__device__ __noinline__ void finalize_warp(const FinArgs a, const double* S, const double* P) {
     __shared__ double Hs[36], gsh[6], scal[2];
     double x[6], Pn[16];
     const int status = solve_pose_warp<METRIC>(S, P, Hs, gsh, scal, x, Pn);
@@ -377,7 +397,7 @@ __device__ __noinline__ void finalize_warp(const IterArgs& a, const double* S, c
 }
 
 template <int METRIC>
-__device__ __noinline__ void finalize(const IterArgs& a, const double* S, const double* P) {
+__device__ __noinline__ void finalize(const FinArgs a, const double* S, const double* P) {
     double H[36], g[6], x[6], Pn[16], sse, cnt;
     const int status = solve_pose<METRIC>(S, P, H, g, x, Pn, sse, cnt);
     if (a.stamps) {
@@ -1087,9 +1107,9 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
         a.stamps[8 * it_stamp + 5] = t;
     }
     if (WARP) {
-        if (threadIdx.x < 32) finalize_warp<METRIC>(a, Ssum, Psh);
+        if (threadIdx.x < 32) finalize_warp<METRIC>(fin_args(a), Ssum, Psh);
     } else if (threadIdx.x == 0) {
-        finalize<METRIC>(a, Ssum, Psh);
+        finalize<METRIC>(fin_args(a), Ssum, Psh);
     }
     if (threadIdx.x == 0) {
         if (a.stamps) {
@@ -1133,8 +1153,11 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
+#ifndef CIL_ACC_MINB
+#define CIL_ACC_MINB 2
+#endif
 template <int METRIC>
-__global__ void __launch_bounds__(kIcpThreads, 2)
+__global__ void __launch_bounds__(kIcpThreads, CIL_ACC_MINB)
 icp_acc_kernel(const IterArgs a) {
     __shared__ double Psh[16];
     pdl_trigger();

@@ -3,8 +3,10 @@
 // cell-offset scan ... chosen by measurement"; index_kind CIL_INDEX_GRID, built by grid.cu).
 //
 // One query per thread.  The search visits shells of cells around the query's own cell:
-// shell r = the cells at Chebyshev distance r.  A cell is evaluated unless its lower bound
-// exceeds the best d^2 so far (ties are never pruned); after shell r every target outside the
+// shell r = the cells at Chebyshev distance r, the first step being the whole 3 x 3 x 3 block
+// (shells 0 and 1) as nine contiguous x-row ranges of the x-major cell order.  A row (a cell
+// of a larger shell) is evaluated unless its lower bound exceeds the best d^2 so far (ties are
+// never pruned); after shell r every target outside the
 // searched block lies beyond its faces, so the search stops as soon as best < (gap to the
 // nearest face not on the grid boundary)^2, or when the block covers the grid.  Queries still
 // unresolved after kGridShells shells finish with the exact per-lane BVH DFS (the BVH is
@@ -59,7 +61,26 @@ __device__ __forceinline__ unsigned long long grid_search(const TargetView& T, c
     const int cz = grid_cell1(s.hz, lh.z, inv_h, nz);
     const float slx = DF ? s.lx : 0.0f, sly = DF ? s.ly : 0.0f, slz = DF ? s.lz : 0.0f;
     bool done = false;
-    for (int r = 0; r <= kGridShells && !done; ++r) {
+    // candidates of the sorted range [a, b) (cells in x-major order: consecutive x cells of a
+    // row are one contiguous range)
+    // (four loads in flight per step; slots past b read a +inf point: key (inf, ~0), never better)
+    auto scan = [&](uint32_t a, uint32_t b) {
+        for (uint32_t j = a; j < b; j += 4) {
+            float4 t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                t[u] = j + u < b ? __ldg(T.gpts + j + u) : make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(~0u));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float dx = DF ? (s.hx - t[u].x) + s.lx : s.hx - t[u].x;
+                const float dy = DF ? (s.hy - t[u].y) + s.ly : s.hy - t[u].y;
+                const float dz = DF ? (s.hz - t[u].z) + s.lz : s.hz - t[u].z;
+                const unsigned long long k = make_key(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), __float_as_uint(t[u].w));
+                best = k < best ? k : best;
+            }
+        }
+    };
+    for (int r = 1; r <= kGridShells && !done; ++r) {
         const int z0 = max(cz - r, 0), z1 = min(cz + r, nz - 1);
         const int y0 = max(cy - r, 0), y1 = min(cy + r, ny - 1);
         for (int z = z0; z <= z1; ++z) {
@@ -69,21 +90,23 @@ __device__ __forceinline__ unsigned long long grid_search(const TargetView& T, c
                 const float gy = grid_gap(s.hy, sly, grid_face_lo(y, lh.y, h, eps), grid_face_hi(y, ny, lh.y, h, eps));
                 const float lrow = fmaf(gy, gy, gz * gz);
                 if (lrow > key_d2(best)) continue;
-                const bool full = zedge || y == cy - r || y == cy + r;   // a face row of the shell
-                const int step = full ? 1 : max(2 * r, 1);
                 const uint32_t* rowp = T.gstart + ((size_t)z * ny + y) * nx;
-                for (int x = cx - r; x <= cx + r; x += step) {
-                    if (x < 0 || x >= nx) continue;
-                    const float gx = grid_gap(s.hx, slx, grid_face_lo(x, lh.x, h, eps), grid_face_hi(x, nx, lh.x, h, eps));
-                    if (fmaf(gx, gx, lrow) > key_d2(best)) continue;
-                    const uint32_t a = __ldg(rowp + x), b = __ldg(rowp + x + 1);
-                    for (uint32_t j = a; j < b; ++j) {
-                        const float4 t = __ldg(T.gpts + j);
-                        const float dx = DF ? (s.hx - t.x) + s.lx : s.hx - t.x;
-                        const float dy = DF ? (s.hy - t.y) + s.ly : s.hy - t.y;
-                        const float dz = DF ? (s.hz - t.z) + s.lz : s.hz - t.z;
-                        const unsigned long long k = make_key(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), __float_as_uint(t.w));
-                        best = k < best ? k : best;
+                const bool full = zedge || y == cy - r || y == cy + r;   // a face row of the shell
+                if (r == 1 || full) {
+                    // shell 1 = the whole 3 x 3 x 3 block (shell 0 included), a face row of a
+                    // larger shell is new in full: one contiguous range per row; the query's
+                    // x lies inside the row's x extent for r = 1 (its lower bound is lrow)
+                    const int xa = max(cx - r, 0), xb = min(cx + r, nx - 1);
+                    scan(__ldg(rowp + xa), __ldg(rowp + xb + 1));
+                } else {
+                    // an inner row of shell r >= 2: only its two end cells are new
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int x = e ? cx + r : cx - r;
+                        if (x < 0 || x >= nx) continue;
+                        const float gx = grid_gap(s.hx, slx, grid_face_lo(x, lh.x, h, eps), grid_face_hi(x, nx, lh.x, h, eps));
+                        if (fmaf(gx, gx, lrow) > key_d2(best)) continue;
+                        scan(__ldg(rowp + x), __ldg(rowp + x + 1));
                     }
                 }
             }

@@ -312,8 +312,8 @@ order_choice_kernel(const float* __restrict__ a, const float* __restrict__ b, in
     const int npk = (n + 31) / 32;
     double ea = 0.0, eb = 0.0;
     for (int pk = blockIdx.x * (kThreads / 32) + warp; pk < npk; pk += gridDim.x * (kThreads / 32)) {
-        ea += log((double)packet_diag(a, 32 * pk, n) + 1e-30);
-        eb += log((double)packet_diag(b, 32 * pk, n) + 1e-30);
+        ea += (double)__logf(packet_diag(a, 32 * pk, n) + 1e-30f);     // (fp32 log: a heuristic, deterministic)
+        eb += (double)__logf(packet_diag(b, 32 * pk, n) + 1e-30f);
     }
     if (lane == 0) { sa[warp] = ea; sb[warp] = eb; }
     __syncthreads();

@@ -314,7 +314,7 @@ constexpr int kItemCap = 256;
 #define CIL_DGROUP 2
 #endif
 #ifndef CIL_TRACE_D
-#define CIL_TRACE_D 1
+#define CIL_TRACE_D 0         // per-query item counts in the engine trace: build a variant with -DCIL_TRACE_D=1
 #endif
 constexpr int kDGroup = CIL_DGROUP;      // frontier leaves tested per step of phase D
 constexpr int kDirectLeaves = CIL_DIRECT_LEAVES;

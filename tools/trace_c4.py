@@ -1,7 +1,8 @@
-"""Engine trace statistics on C4 (GPU box): per-query packet phases at the identity and the
+"""(Item counts need a trace build: tools/variants.sh trace "-DCIL_TRACE_D=1", then PYTHONPATH=tools/ubench/var_trace.)
+Engine trace statistics on C4 (GPU box): per-query packet phases at the identity and the
 ground-truth pose (stateless iterate, cold hints) and in a warm run (iteration k)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))   # (a variant on PYTHONPATH wins)
 import numpy as np, torch
 import gen, paper_1807_00399_b200 as cil
 from scipy.spatial.transform import Rotation

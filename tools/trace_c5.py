@@ -1,7 +1,8 @@
-"""Engine trace statistics on C5 (GPU box): per-query packet phases of the stateless iterate at
+"""(Item counts need a trace build: tools/variants.sh trace "-DCIL_TRACE_D=1", then PYTHONPATH=tools/ubench/var_trace.)
+Engine trace statistics on C5 (GPU box): per-query packet phases of the stateless iterate at
 the identity for 2^20 and 2^22 points (cold hints)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))   # (a variant on PYTHONPATH wins)
 import numpy as np, torch
 import gen, paper_1807_00399_b200 as cil
 

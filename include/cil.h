@@ -329,7 +329,8 @@ cil_status cil_debug_set_cert_skin(double min_frac, double max_frac, double kapp
 /* Diagnostics: while buf (device int32, >= 16 per query slot) is non-NULL, every search-engine
    launch writes per processed query slot {flags, r, i0, i1, nF, best d2 after the packet
    phases, work items, final best d2, SM clocks of phases A, B, C, D+E, F, 0, 0, 0}.  NULL
-   switches it off.  Host-only, process-wide. */
+   switches it off.  Host-only, process-wide.  Only a library built with -DCIL_TRACE=1 traces
+   (the default build returns CIL_ERR_INVALID_ARG for a non-NULL buf). */
 cil_status cil_debug_engine_trace(int32_t* buf);
 
 /* Diagnostics: while buf (device uint64, 8 per iteration, filled with 0xff by the caller) is

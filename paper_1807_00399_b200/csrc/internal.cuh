@@ -12,6 +12,12 @@
 
 #define CIL_API extern "C" __attribute__((visibility("default")))
 
+// The diagnostic engine trace (cil_debug_engine_trace) exists only in a build with -DCIL_TRACE=1
+// (tools/variants.sh): its bookkeeping costs the search kernels registers (spills) and time.
+#ifndef CIL_TRACE
+#define CIL_TRACE 0
+#endif
+
 // Largest grid the reduction workspace is sized for (148 SMs x 8 resident CTAs).
 constexpr int kMaxCtas = 1184;
 // Doubles per per-CTA partial (the 29 point-to-plane / 17 point-to-point sums, padded).

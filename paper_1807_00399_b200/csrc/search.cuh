@@ -314,7 +314,7 @@ constexpr int kItemCap = 256;
 #define CIL_DGROUP 2
 #endif
 #ifndef CIL_TRACE_D
-#define CIL_TRACE_D 0         // per-query item counts in the engine trace: build a variant with -DCIL_TRACE_D=1
+#define CIL_TRACE_D CIL_TRACE // (per-query item counts in that trace)
 #endif
 constexpr int kDGroup = CIL_DGROUP;      // frontier leaves tested per step of phase D
 constexpr int kDirectLeaves = CIL_DIRECT_LEAVES;
@@ -541,7 +541,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         if (c >= npk) break;
         const int base = qs.packet_base(c);
         const int qi = base + lane;
-        const bool tracing = T.trace != nullptr;
+        const bool tracing = CIL_TRACE && T.trace != nullptr;
         unsigned ck0 = tracing ? (unsigned)clock() : 0u, ckA = 0, ckB = 0, ckC = 0, ckD = 0;
         DF3 s;
         unsigned long long best = 0ull;
@@ -801,7 +801,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             }
         }
         if (tracing) { ckD = (unsigned)clock(); if (!ckC) ckC = ckD; }
-        int* trace = T.trace;
+        int* trace = CIL_TRACE ? T.trace : nullptr;
         if (trace && qi < m) {
             int* rec = trace + 16 * (size_t)qi;
             rec[0] = normal | (outlier << 1) | (overflow << 2) | (sparse << 3);

@@ -1,4 +1,4 @@
-"""(Item counts need a trace build: tools/variants.sh trace "-DCIL_TRACE_D=1", then PYTHONPATH=tools/ubench/var_trace.)
+"""(Needs a trace build: tools/variants.sh trace "-DCIL_TRACE=1", then PYTHONPATH=tools/ubench/var_trace.)
 Engine trace statistics on C4 (GPU box): per-query packet phases at the identity and the
 ground-truth pose (stateless iterate, cold hints) and in a warm run (iteration k)."""
 import sys, os

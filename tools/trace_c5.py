@@ -1,4 +1,4 @@
-"""(Item counts need a trace build: tools/variants.sh trace "-DCIL_TRACE_D=1", then PYTHONPATH=tools/ubench/var_trace.)
+"""(Needs a trace build: tools/variants.sh trace "-DCIL_TRACE=1", then PYTHONPATH=tools/ubench/var_trace.)
 Engine trace statistics on C5 (GPU box): per-query packet phases of the stateless iterate at
 the identity for 2^20 and 2^22 points (cold hints)."""
 import sys, os

@@ -557,7 +557,6 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         }
         if (!__any_sync(FULL, active)) continue;                 // nothing to search in this packet
         if (!active) { s.hx = s.hy = s.hz = 0.0f; s.lx = s.ly = s.lz = 0.0f; best = 0ull; hint = -1; }
-        const NegQuery nq = neg_query(s);
         const float cap2 = key_d2(best);                      // the search bound (rho^2 / max^2 / inf)
         auto thr_of = [&](unsigned long long b) {
             const float d = key_d2(b);
@@ -569,12 +568,12 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         float sec = INFINITY;                                 // CERT: leaf-level 2nd best
         int hint2 = -1;                                       // second hint leaf (cold), or -1
         if (active) {
-            eval_leaf_seq<B, CERT>(T, nq, hint, best, sec);
+            eval_leaf_seq<B, CERT>(T, neg_query(s), hint, best, sec);
             // a warm hint that went stale (large early ICP steps): also try the leaf that
             // follows the query's own Morton key, and keep the better of the two
             if (warm && key_d2(best) > stale2) {
                 hint2 = coarse_hint_leaf(T, s);
-                if (hint2 != hint) eval_leaf_seq<B, CERT>(T, nq, hint2, best, sec);
+                if (hint2 != hint) eval_leaf_seq<B, CERT>(T, neg_query(s), hint2, best, sec);
                 else hint2 = -1;
             }
         }
@@ -628,13 +627,14 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         }
         const float rcap = CIL_RCAP * rsum / (float)max(na, 1);
         bool normal = active && r <= rcap && r < INFINITY;
-        if (T.dbg_mode == 1) normal = false;
-        if (T.dbg_mode == 2) normal = active && r < INFINITY;
+        const int dbg_mode = CIL_TRACE ? T.dbg_mode : 0;       // (diagnostic engine modes: trace builds)
+        if (dbg_mode == 1) normal = false;
+        if (dbg_mode == 2) normal = active && r < INFINITY;
         // an outlier (radius above the cap) joins the packet with its ball capped at rcap: if its
         // nearest neighbour lies within the cap the packet phases find it exactly, otherwise it
         // finishes with the ballot DFS
         const bool outlier = active && !normal;
-        const bool capped = outlier && r < INFINITY && T.dbg_mode == 0;
+        const bool capped = outlier && r < INFINITY && dbg_mode == 0;
         const float rcap2 = rcap * rcap;
         if (CERT && capped) sThr[wid][lane] = fminf(thr, rcap2);     // list appends stop at the cap
         const bool inP = normal || capped;
@@ -784,7 +784,7 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
 #pragma unroll
                     for (int u = 0; u < kDGroup; ++u) f[u] = k + u < nF ? F[k + u] : -1;
 #pragma unroll
-                    for (int u = 0; u < kDGroup; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, nq, f[u]) : INFINITY;
+                    for (int u = 0; u < kDGroup; ++u) lb[u] = f[u] >= 0 ? leaf_lb2(T, neg_query(s), f[u]) : INFINITY;
                     const float lim = capped ? fminf(thr, rcap2) : thr;
 #pragma unroll
                     for (int u = 0; u < kDGroup; ++u) {
@@ -825,9 +825,9 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             int cnt = 0;
             int* lst = nullptr;
             if constexpr (CERT) { drop = sDrop[wid][lane]; cnt = sCnt[wid][lane]; lst = sList[wid][lane]; }
-            if (lane_on) lane_dfs<B, CERT>(T, s, nq, hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
+            if (lane_on) lane_dfs<B, CERT>(T, s, neg_query(s), hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
             if (__any_sync(FULL, ballot_on))
-                ballot_dfs<B, CERT>(T, s, nq, ballot_on, hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
+                ballot_dfs<B, CERT>(T, s, neg_query(s), ballot_on, hint, hint2, g, cap2, best, sec, lst, &cnt, &drop);
             if constexpr (CERT) { sDrop[wid][lane] = drop; sCnt[wid][lane] = cnt; }
             if (active && (lane_on || ballot_on)) thr = thr_of(best);
         }

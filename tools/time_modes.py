@@ -1,8 +1,9 @@
-"""Engine timings under the diagnostic engine modes (cil_debug_set_flags bits 1-2): 0 = packet
+"""(Modes 1-2 need a trace build: tools/variants.sh trace "-DCIL_TRACE=1", then PYTHONPATH=tools/ubench/var_trace.)
+Engine timings under the diagnostic engine modes (cil_debug_set_flags bits 1-2): 0 = packet
 phases, 1 = every lane through the ballot DFS, 2 = no outlier cap.  C4 iterate at the identity and
 the ground truth, C2 BVH query, C5 2^20 / 2^22 iterate (L2 flushed, median of 5)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import gen, paper_1807_00399_b200 as cil
 

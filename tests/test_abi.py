@@ -175,3 +175,13 @@ def test_voxel_argument_errors(cil):
     assert L.cil_voxel_downsample(fake, None, 10, 0.01, None, fake, None, None, None) == cil.CIL_ERR_INVALID_ARG
     assert L.cil_voxel_downsample(None, None, 10, 0.01, None, fake, None, fake, None) == cil.CIL_ERR_INVALID_ARG
     assert L.cil_voxel_downsample(fake, None, 10, 0.01, None, fake, fake, fake, None) == cil.CIL_ERR_NO_NORMALS
+
+
+def test_engine_trace_needs_a_trace_build(cil):
+    """The default build compiles the diagnostic engine trace out (include/cil.h): a non-NULL
+    buffer is refused with CIL_ERR_INVALID_ARG and a message; NULL (off) is accepted."""
+    buf = (C.c_int32 * 64)()
+    rc = cil.lib().cil_debug_engine_trace(C.cast(buf, C.c_void_p))
+    assert rc == cil.CIL_ERR_INVALID_ARG
+    assert b"CIL_TRACE" in cil.lib().cil_last_error()
+    assert cil.lib().cil_debug_engine_trace(None) == cil.CIL_OK

@@ -1644,9 +1644,8 @@ __global__ void reset_ticket_kernel(IcpState* st) { st->ticket = 0; st->work = 0
 #define CIL_CARVE_ACC 0
 #endif
 template <class K>
-int set_carve(K kernel, int pct) {
+void set_carve(K kernel, int pct) {
     if (pct >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    return 0;
 }
 
 template <class K>
@@ -1664,8 +1663,8 @@ inline int persistent_grid(int occ, int threads, int m, int cap_ctas) {
 
 template <int B, bool CERT>
 cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
-    static const int carve = set_carve(icp_nn_kernel<B, CERT>, CIL_CARVE_NN);
-    static const int occ = occupancy_of(icp_nn_kernel<B, CERT>, kNNThreads) + carve;
+    // (the carveout is set before the occupancy is queried)
+    static const int occ = (set_carve(icp_nn_kernel<B, CERT>, CIL_CARVE_NN), occupancy_of(icp_nn_kernel<B, CERT>, kNNThreads));
     const int g = persistent_grid(occ, kNNThreads, a.m, 1 << 20);
     prof_begin(kProfNN, s);
     IterArgs ad = a;
@@ -1704,8 +1703,7 @@ cudaError_t launch_nn_t(const IterArgs& a, cudaStream_t s) {
 
 template <int METRIC>
 cudaError_t launch_acc_m(const IterArgs& a, cudaStream_t s) {
-    static const int carve = set_carve(icp_acc_kernel<METRIC>, CIL_CARVE_ACC);
-    static const int occ = occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads) + carve;
+    static const int occ = (set_carve(icp_acc_kernel<METRIC>, CIL_CARVE_ACC), occupancy_of(icp_acc_kernel<METRIC>, kIcpThreads));
     const int g = persistent_grid(occ, kIcpThreads, a.m, kMaxCtas);
     prof_begin(kProfAcc, s);
     cudaError_t e = launch_pdl(icp_acc_kernel<METRIC>, g, kIcpThreads, s, a);
@@ -1720,26 +1718,21 @@ cudaError_t launch_iter(const IterArgs& a0, int metric, cudaStream_t s) {
     cudaError_t e0 = cudaSuccess;
     int n = 2;
     if (a.cert) {
-        int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
-#if CIL_SEL_PERSIST
-        // the certificate kernel's evaluations re-read leaves through L1, the accumulation's
-        // gathers too: both run with the smallest shared-memory carveout that keeps their
-        // occupancy (measured: C4 run 14.52 -> 14.34 ms)
-        static const int occ_sel = [] {
-            set_carve(icp_select_kernel<4>, CIL_CARVE_SEL);
-            set_carve(icp_select_kernel<8>, CIL_CARVE_SEL);
-            set_carve(icp_select_kernel<16>, CIL_CARVE_SEL);
-            set_carve(icp_select_kernel<32>, CIL_CARVE_SEL);
-            return occupancy_of(icp_select_kernel<16>, kSelThreads);
-        }();
-        g = std::min(g, occ_sel * sm_count());
-#endif
+        const int g = std::max(1, (a.m + kSelTile - 1) / kSelTile);
+        // persistent grid: the resident CTAs per SM of the instance launched.  The certificate
+        // kernel's evaluations re-read leaves through L1, the accumulation's gathers too: both run
+        // with the smallest shared-memory carveout that keeps their occupancy (measured: C4 run
+        // 14.52 -> 14.34 ms)
+        auto persist = [&](int occ) { return CIL_SEL_PERSIST ? std::min(g, occ * sm_count()) : g; };
+        auto occ_of = [](auto kernel) { set_carve(kernel, CIL_CARVE_SEL); return occupancy_of(kernel, kSelThreads); };
+        static const int occ4 = occ_of(icp_select_kernel<4>), occ8 = occ_of(icp_select_kernel<8>),
+                         occ16 = occ_of(icp_select_kernel<16>), occ32 = occ_of(icp_select_kernel<32>);
         prof_begin(kProfSel, s);
         switch (a.T.leaf_size) {
-            case 4: e0 = launch_pdl(icp_select_kernel<4>, g, kSelThreads, s, a); break;
-            case 8: e0 = launch_pdl(icp_select_kernel<8>, g, kSelThreads, s, a); break;
-            case 16: e0 = launch_pdl(icp_select_kernel<16>, g, kSelThreads, s, a); break;
-            default: e0 = launch_pdl(icp_select_kernel<32>, g, kSelThreads, s, a); break;
+            case 4: e0 = launch_pdl(icp_select_kernel<4>, persist(occ4), kSelThreads, s, a); break;
+            case 8: e0 = launch_pdl(icp_select_kernel<8>, persist(occ8), kSelThreads, s, a); break;
+            case 16: e0 = launch_pdl(icp_select_kernel<16>, persist(occ16), kSelThreads, s, a); break;
+            default: e0 = launch_pdl(icp_select_kernel<32>, persist(occ32), kSelThreads, s, a); break;
         }
         prof_end(s);
         if (e0 != cudaSuccess) return e0;

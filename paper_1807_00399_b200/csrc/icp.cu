@@ -459,6 +459,9 @@ __device__ __forceinline__ float displacement_bound(const float* __restrict__ D,
 // a full search; K_nn then runs its packets in source order with only those lanes active, so
 // an uncertified remainder stays spatially coherent (a compacted list would scatter it).
 constexpr int kSelThreads = 256;
+#ifndef CIL_SEL_PREFETCH
+#define CIL_SEL_PREFETCH 1     // a queued record's candidate list prefetched at classification (C4 run -0.4 %)
+#endif
 #ifndef CIL_SEL_ROUNDS
 #define CIL_SEL_ROUNDS 4
 #endif
@@ -565,6 +568,10 @@ __device__ __forceinline__ bool classify(const IterArgs& a, int i, const SelIn& 
                 } else {
                     eval = true;
                     rec = (uint32_t)i | (leaf_ok ? 0x80000000u : 0u);
+#if CIL_SEL_PREFETCH
+                    // its candidate-leaf list is read by the evaluation step: start the fetch now
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.vlist + (size_t)kListLeaves * i));
+#endif
                     // targets outside the evaluated leaves were >= d_out (resp. r_S) from the anchor
                     outer = (leaf_ok ? G1 : GS) + in.gd1 - D;
                 }

@@ -1160,6 +1160,9 @@ __device__ __forceinline__ void solve_tail(const IterArgs& a, const double* Ssum
 }
 
 // ---------------------------------------------------------------- K_acc (+ a6, a7)
+#ifndef CIL_ACC_PREFETCH
+#define CIL_ACC_PREFETCH 2     // next trip's matches / source (1), and its gathers (2) prefetched
+#endif
 #ifndef CIL_ACC_MINB
 #define CIL_ACC_MINB 2
 #endif
@@ -1187,15 +1190,49 @@ icp_acc_kernel(const IterArgs a) {
     // nn[]; four independent chains in flight per thread); summation order = grid-stride order
     constexpr int U = 4;
     const int stride = gridDim.x * blockDim.x;
+#if CIL_ACC_PREFETCH >= 2
+    int jn[U];                                   // the matches of the next trip (one trip ahead)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int iu = blockIdx.x * blockDim.x + threadIdx.x + u * stride;
+        jn[u] = iu < a.m ? a.nn[iu] : -1;
+    }
+#endif
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += U * stride) {
         int jj[U];
         float4 tt[U], nn4[U];
         float px[U], py[U], pz[U];
+#if CIL_ACC_PREFETCH >= 2
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            jj[u] = jn[u];
+            const int iu = i + (U + u) * stride;
+            jn[u] = iu < a.m ? a.nn[iu] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + (2 * U + u) * stride;
+            if (iu < a.m) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.nn + iu));
+        }
+#else
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int iu = i + u * stride;
             jj[u] = iu < a.m ? a.nn[iu] : -1;
         }
+#endif
+#if CIL_ACC_PREFETCH
+        // the next trip's matches and source points: their fetch overlaps this trip's gathers
+        // (prefetch, no registers held)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int iu = i + (U + u) * stride;
+            if (iu < a.m) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.nn + iu));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src + 3 * (size_t)iu));
+            }
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int iu = i + u * stride;
@@ -1208,6 +1245,14 @@ icp_acc_kernel(const IterArgs a) {
                 px[u] = a.src[3 * (size_t)iu]; py[u] = a.src[3 * (size_t)iu + 1]; pz[u] = a.src[3 * (size_t)iu + 2];
             }
         }
+#if CIL_ACC_PREFETCH >= 2
+#pragma unroll
+        for (int u = 0; u < U; ++u)                                    // the next trip's gathers
+            if (jn[u] >= 0) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(T.opts + jn[u]));
+                if (METRIC != CIL_POINT_TO_POINT) asm volatile("prefetch.global.L1 [%0];" ::"l"(T.onrm + jn[u]));
+            }
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u)                                    // a3: nn < 0 = nothing within the bound
             if (jj[u] >= 0) accumulate_pair<METRIC>(acc, P, px[u], py[u], pz[u], tt[u], nn4[u], a.bound2, a.w_pp, a.w_pl);

@@ -1,6 +1,6 @@
 """C1 (4,096-point sphere, 20 iterations) run and iterate timing, small path vs tree path."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import gen, paper_1807_00399_b200 as cil
 w = gen.c1_sphere()

@@ -83,7 +83,7 @@ typedef enum {
 
 /* Spatial-index parameters (NULL = defaults).  leaf_size: points per BVH leaf
    (0 = default 16; 4, 8, 16 or 32).  index_kind: cil_index_kind.  grid_points: mean target
-   points per grid cell over the bounding box (0 = default 2; CIL_INDEX_GRID only; > 0 and
+   points per grid cell over the bounding box (0 = default 1; CIL_INDEX_GRID only; > 0 and
    finite).  Other fields reserved, must be 0. */
 typedef struct {
     int32_t leaf_size;

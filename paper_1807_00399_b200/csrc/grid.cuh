@@ -28,6 +28,9 @@
 namespace cil {
 
 constexpr int kGridShells = 2;      // shells searched on the grid before the BVH fallback
+#ifndef CIL_GRID_W
+#define CIL_GRID_W 4                // candidate loads in flight per step of a row scan
+#endif
 
 __device__ __forceinline__ float grid_face_lo(int c, float lo, float h, float eps) {
     return c <= 0 ? -INFINITY : fmaf((float)c, h, lo) - eps;
@@ -65,13 +68,14 @@ __device__ __forceinline__ unsigned long long grid_search(const TargetView& T, c
     // row are one contiguous range)
     // (four loads in flight per step; slots past b read a +inf point: key (inf, ~0), never better)
     auto scan = [&](uint32_t a, uint32_t b) {
-        for (uint32_t j = a; j < b; j += 4) {
-            float4 t[4];
+        constexpr int W = CIL_GRID_W;
+        for (uint32_t j = a; j < b; j += W) {
+            float4 t[W];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < W; ++u)
                 t[u] = j + u < b ? __ldg(T.gpts + j + u) : make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(~0u));
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < W; ++u) {
                 const float dx = DF ? (s.hx - t[u].x) + s.lx : s.hx - t[u].x;
                 const float dy = DF ? (s.hy - t[u].y) + s.ly : s.hy - t[u].y;
                 const float dz = DF ? (s.hz - t[u].z) + s.lz : s.hz - t[u].z;

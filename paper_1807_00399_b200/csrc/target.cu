@@ -447,7 +447,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     if (!pts) { set_error("cil_target_build: pts is NULL"); return CIL_ERR_INVALID_ARG; }
     int B = 16;                 // default leaf size (measured over C1-C5)
     int kind = CIL_INDEX_BVH;
-    float grid_points = 2.0f;   // targets per grid cell
+    float grid_points = 1.0f;   // targets per grid cell (1 beats 2 on C2 since the row-range search)
     if (params) {
         if (params->leaf_size) B = params->leaf_size;
         kind = params->index_kind;

@@ -84,17 +84,12 @@ typedef enum {
 /* Spatial-index parameters (NULL = defaults).  leaf_size: points per BVH leaf
    (0 = default 16; 4, 8, 16 or 32).  index_kind: cil_index_kind.  grid_points: mean target
    points per grid cell over the bounding box (0 = default 1; CIL_INDEX_GRID only; > 0 and
-   finite).  leaf_lists: leaf neighbour lists -- for every BVH leaf the
-   leaf_lists nearest other leaves by box distance, sorted, plus a cut below which the list is
-   complete; a query whose ball around its hint leaf stays inside the cut is resolved by
-   scanning that list (exact; others take the packet engine).  0 = default (64), -1 = none,
-   else 1 .. 256 entries.  Other fields reserved, must be 0. */
+   finite).  Other fields reserved, must be 0. */
 typedef struct {
     int32_t leaf_size;
     int32_t index_kind;
     float grid_points;
-    int32_t leaf_lists;
-    int32_t reserved[4];
+    int32_t reserved[5];
 } cil_index_params;
 
 /* ICP parameters.  metric: cil_metric.  max_iters >= 1 (cil_icp_run only).

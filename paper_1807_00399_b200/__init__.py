@@ -55,7 +55,7 @@ EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_n
 
 class cil_index_params(C.Structure):
     _fields_ = [("leaf_size", C.c_int32), ("index_kind", C.c_int32), ("grid_points", C.c_float),
-                ("leaf_lists", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("reserved", C.c_int32 * 5)]
 
 
 class cil_icp_params(C.Structure):
@@ -308,7 +308,7 @@ class Target:
 
 
 def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, leaf_size: int = 0,
-                     stream=None, index: str = "bvh", grid_points: float = 0.0, leaf_lists: int = 0) -> Target:
+                     stream=None, index: str = "bvh", grid_points: float = 0.0) -> Target:
     _pts(pts, "pts")
     if normals is not None:
         _pts(normals, "normals")
@@ -318,7 +318,6 @@ def cil_target_build(pts: torch.Tensor, normals: torch.Tensor | None = None, lea
     prm.leaf_size = int(leaf_size)
     prm.index_kind = {"bvh": CIL_INDEX_BVH, "grid": CIL_INDEX_GRID}[index]
     prm.grid_points = float(grid_points)
-    prm.leaf_lists = int(leaf_lists)
     h = _vp()
     _check(_lib.cil_target_build(_ptr(pts), _ptr(normals), pts.shape[0], C.byref(prm), _stream_ptr(stream),
                                  C.byref(h)), "cil_target_build")

@@ -1722,7 +1722,6 @@ cudaError_t launch_nn_b(const IterArgs& a, cudaStream_t s) {
     IterArgs ad = a;
     ad.T.trace = debug_trace();
     ad.T.dbg_mode = (int)(debug_flags() >> 1) & 3;
-    if (debug_flags() & 128u) ad.T.lnl = nullptr;     // diagnostics bit 7: search without the leaf lists
     cudaError_t e = launch_pdl(icp_nn_kernel<B, CERT>, g, kNNThreads, s, ad);
     prof_end(s);
     return e;

@@ -22,8 +22,6 @@
 constexpr int kMaxCtas = 1184;
 // Doubles per per-CTA partial (the 29 point-to-plane / 17 point-to-point sums, padded).
 constexpr int kSlots = 32;
-// Leaf neighbour list length of the default index (lnl.cu).
-constexpr int kDefaultLeafLists = 64;
 // Morton bits per axis (48-bit keys -> 6 radix passes of 8 bits).
 constexpr int kMortonBits = 16;
 
@@ -56,9 +54,6 @@ struct TargetView {
     const float4* gpts;   // grid: [n] points sorted by cell (x, y, z, original index bits), or nullptr
     const uint32_t* gstart;  // grid: [cells + 1] first sorted position of every cell
     const GridDesc* gdesc;   // grid: descriptor (device)
-    const int2* lnl;      // leaf neighbour lists (lnl.cu): [n_leaves * lnl_k] (leaf, dist bits) sorted, or nullptr
-    const float* lnl_cut; // [n_leaves]: every leaf outside the list of h is at real box distance >= lnl_cut[h]
-    int lnl_k;
     int* trace;           // diagnostics only (cil_debug_engine_trace), normally nullptr
     int dbg_mode;         // diagnostics only (cil_debug_set_flags bits 1-2), normally 0
 };
@@ -71,7 +66,6 @@ struct cil_target {
     int device;
     void* mem;            // single stream-ordered allocation holding pts / nrm / box
     void* gmem;           // the grid's allocation (CIL_INDEX_GRID) or nullptr
-    void* lmem;           // the leaf neighbour lists' allocation or nullptr
     size_t bytes;
 };
 
@@ -166,10 +160,6 @@ cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long
 // written by the build); allocates from the pool into *mem (owned by the target afterwards)
 cudaError_t grid_build(const float* pts, int n, const float4* quant, const float4* qmax, float pts_per_cell,
                        cudaStream_t s, void** mem, size_t* bytes, TargetView* v, int* nlaunch);
-
-// lnl.cu: leaf neighbour lists (K per leaf) built from the finished BVH into mem
-size_t lnl_bytes(int64_t n_leaves, int K);
-cudaError_t lnl_build(const float4* box, int l_pad, int64_t n_leaves, int K, void* mem, cudaStream_t s, TargetView* v);
 
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);

@@ -91,7 +91,6 @@ cudaError_t launch_nn(const TargetView& T, const NNQueries& qs, int m, unsigned 
     TargetView Tv = T;
     Tv.trace = debug_trace();
     Tv.dbg_mode = (int)(debug_flags() >> 1) & 3;
-    if (debug_flags() & 128u) Tv.lnl = nullptr;       // diagnostics bit 7: search without the leaf lists
     if (T.gpts) {
         grid_query_kernel<B><<<(int)(((int64_t)m + kNNThreads - 1) / kNNThreads), kNNThreads, 0, s>>>(Tv, qs, m);
         count_launches(1);

@@ -179,10 +179,9 @@ __device__ __forceinline__ uint32_t leaf_argmin(const TargetView& T, int leaf, c
 // best <- min(best, key of the leaf's nearest candidate); CERT: sec <- the smallest leaf
 // minimum of any OTHER leaf (the value that loses against the running best is pushed:
 // sec <- min(sec, max(best_d2, m1)))
-// (returns the leaf's minimum d2)
 template <int B, bool CERT>
-__device__ __forceinline__ float eval_leaf_seq(const TargetView& T, const NegQuery& q, int leaf,
-                                               unsigned long long& best, float& sec) {
+__device__ __forceinline__ void eval_leaf_seq(const TargetView& T, const NegQuery& q, int leaf,
+                                              unsigned long long& best, float& sec) {
     float d2[B];
     leaf_d2<B>(T, q, leaf, d2);
     const float m1 = leaf_min<B>(d2);
@@ -194,7 +193,6 @@ __device__ __forceinline__ float eval_leaf_seq(const TargetView& T, const NegQue
     } else if (CERT) {
         sec = fminf(sec, m1);
     }
-    return m1;
 }
 
 // work-item evaluation (any lane, for a query slot in shared memory): atomicMin on the
@@ -569,9 +567,8 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
         // ---- A
         float sec = INFINITY;                                 // CERT: leaf-level 2nd best
         int hint2 = -1;                                       // second hint leaf (cold), or -1
-        float m1h = INFINITY;                                 // the hint leaf's minimum d2
         if (active) {
-            m1h = eval_leaf_seq<B, CERT>(T, neg_query(s), hint, best, sec);
+            eval_leaf_seq<B, CERT>(T, neg_query(s), hint, best, sec);
             // a warm hint that went stale (large early ICP steps): also try the leaf that
             // follows the query's own Morton key, and keep the better of the two
             if (warm && key_d2(best) > stale2) {
@@ -618,68 +615,25 @@ __device__ __forceinline__ void nn_packet_engine(const TargetView& T, Q& qs, int
             sDrop[wid][lane] = __float_as_uint(INFINITY);
             sThr[wid][lane] = thr;
         }
-        // ---- L: per-query leaf-list search (lnl.cu): every target x inside the ball B(s, r)
-        // lies within r + dist(s, box(hint)) of the hint leaf's box, so if that is below the
-        // hint leaf's cut, every leaf that can hold a target within the threshold is in the
-        // hint leaf's list, sorted by box distance: scan it up to the first entry beyond
-        // r + dist(s, box(hint)) (both rounded up: sqrt(m1h) bounds the real distance to the box
-        // up to the fp32 d2 error, covered by the 2e-5 relative and the absolute margins).
-        bool ldone = false;
-        if (T.lnl != nullptr && active && hint >= 0 && best != bound_key(cap2)) {
-            const float amarg = 1e-7f * (1.0f + fmaxf(fabsf(s.hx), fmaxf(fabsf(s.hy), fabsf(s.hz))));
-            const float sh = sqrtf(m1h) * 1.00002f + amarg;
-            if (sqrtf(thr) * 1.00002f + sh < __ldg(T.lnl_cut + hint)) {
-                ldone = true;
-                int cnt = 0;
-                unsigned drop = 0u;
-                int* lst = nullptr;
-                if constexpr (CERT) { cnt = sCnt[wid][lane]; drop = sDrop[wid][lane]; lst = sList[wid][lane]; }
-                const int2* L = T.lnl + (size_t)hint * T.lnl_k;
-                const NegQuery nq = neg_query(s);
-                for (int e = 0; e < T.lnl_k; ++e) {
-                    const int2 E = __ldg(L + e);
-                    if (E.x < 0 || __int_as_float(E.y) > sqrtf(thr) * 1.00002f + sh) break;
-                    if (E.x == hint2 || leaf_lb2(T, nq, E.x) > thr) continue;
-                    float d2[B];
-                    leaf_d2<B>(T, nq, E.x, d2);
-                    const float m1 = leaf_min<B>(d2);
-                    if (CERT && m1 <= thr) {
-                        if (cnt < kListLeaves) lst[cnt] = E.x;
-                        else drop = min(drop, __float_as_uint(m1));
-                        ++cnt;
-                    }
-                    if (m1 <= key_d2(best)) {
-                        const unsigned long long k = make_key(m1, leaf_argmin<B>(T, E.x, d2, m1));
-                        if (CERT && k != best) sec = fminf(sec, fmaxf(key_d2(best), m1));
-                        if (k < best) best = k;
-                    } else if (CERT) {
-                        sec = fminf(sec, m1);
-                    }
-                    thr = thr_of(best);
-                }
-                if constexpr (CERT) { sCnt[wid][lane] = cnt; sDrop[wid][lane] = drop; sThr[wid][lane] = thr; }
-            }
-        }
-        const bool eng = active && !ldone;                   // lanes left to the packet engine
         if (tracing) ckA = (unsigned)clock();
         // ---- B: outliers and the packet box
-        const float r = eng ? sqrtf(thr) : 0.0f;
+        const float r = active ? sqrtf(thr) : 0.0f;
         float rsum = r;
-        int na = eng ? 1 : 0;
+        int na = active ? 1 : 0;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             rsum += __shfl_xor_sync(FULL, rsum, o);
             na += __shfl_xor_sync(FULL, na, o);
         }
         const float rcap = CIL_RCAP * rsum / (float)max(na, 1);
-        bool normal = eng && r <= rcap && r < INFINITY;
+        bool normal = active && r <= rcap && r < INFINITY;
         const int dbg_mode = CIL_TRACE ? T.dbg_mode : 0;       // (diagnostic engine modes: trace builds)
         if (dbg_mode == 1) normal = false;
-        if (dbg_mode == 2) normal = eng && r < INFINITY;
+        if (dbg_mode == 2) normal = active && r < INFINITY;
         // an outlier (radius above the cap) joins the packet with its ball capped at rcap: if its
         // nearest neighbour lies within the cap the packet phases find it exactly, otherwise it
         // finishes with the ballot DFS
-        const bool outlier = eng && !normal;
+        const bool outlier = active && !normal;
         const bool capped = outlier && r < INFINITY && dbg_mode == 0;
         const float rcap2 = rcap * rcap;
         if (CERT && capped) sThr[wid][lane] = fminf(thr, rcap2);     // list appends stop at the cap

@@ -448,17 +448,11 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     int B = 16;                 // default leaf size (measured over C1-C5)
     int kind = CIL_INDEX_BVH;
     float grid_points = 1.0f;   // targets per grid cell (1 beats 2 on C2 since the row-range search)
-    int K = kDefaultLeafLists;  // leaf neighbour list length
     if (params) {
         if (params->leaf_size) B = params->leaf_size;
         kind = params->index_kind;
         if (params->grid_points != 0.0f) grid_points = params->grid_points;
-        if (params->leaf_lists) K = params->leaf_lists < 0 ? 0 : params->leaf_lists;
-        if (params->leaf_lists < -1 || params->leaf_lists > 256) {
-            set_error("cil_target_build: leaf_lists %d not in {-1, 0 .. 256}", params->leaf_lists);
-            return CIL_ERR_INVALID_ARG;
-        }
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 5; ++k)
             if (params->reserved[k]) { set_error("cil_target_build: reserved index params must be 0"); return CIL_ERR_INVALID_ARG; }
     }
     if (kind != CIL_INDEX_BVH && kind != CIL_INDEX_GRID) {
@@ -558,14 +552,6 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
         first >>= lv;
         rem -= lv;
     }
-    TargetView lv{};
-    void* lmem = nullptr;
-    if (K > 0 && e == cudaSuccess) {
-        e = pool_alloc(&lmem, lnl_bytes(n_leaves, K), s);
-        if (e == cudaSuccess) e = lnl_build(d_box, (int)l_pad, n_leaves, K, lmem, s, &lv);
-        else lmem = nullptr;
-        nlaunch += 1;
-    }
     TargetView gv{};
     void* gmem = nullptr;
     size_t gbytes = 0;
@@ -581,7 +567,6 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     if (e != cudaSuccess) {
         pool_free(mem, s);
         if (gmem) pool_free(gmem, s);
-        if (lmem) pool_free(lmem, s);
         return cuda_fail(e, "cil_target_build launch");
     }
 
@@ -590,10 +575,6 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     t->v.gstart = gv.gstart;
     t->v.gdesc = gv.gdesc;
     t->gmem = gmem;
-    t->lmem = lmem;
-    t->v.lnl = lv.lnl;
-    t->v.lnl_cut = lv.lnl_cut;
-    t->v.lnl_k = lmem ? K : 0;
     t->index_kind = kind;
     t->v.opts = d_pts;
     t->v.onrm = d_nrm;
@@ -614,7 +595,7 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     t->has_normals = normals ? 1 : 0;
     t->device = dev;
     t->mem = mem;
-    t->bytes = bytes + gbytes + (lmem ? lnl_bytes(n_leaves, K) : 0);
+    t->bytes = bytes + gbytes;
     *out = t;
     return CIL_OK;
 }
@@ -624,10 +605,6 @@ CIL_API cil_status cil_target_free(cil_target* t, cil_stream_t stream) {
     cudaError_t e = pool_free(t->mem, (cudaStream_t)stream);
     if (t->gmem) {
         const cudaError_t e2 = pool_free(t->gmem, (cudaStream_t)stream);
-        if (e == cudaSuccess) e = e2;
-    }
-    if (t->lmem) {
-        const cudaError_t e2 = pool_free(t->lmem, (cudaStream_t)stream);
         if (e == cudaSuccess) e = e2;
     }
     delete t;

@@ -147,6 +147,23 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// the same launch with or without the attribute (pdl = false: an ordinary stream-ordered launch;
+// the kernels' griddepcontrol instructions are then no-ops)
+template <class... KArgs, class... Args>
+cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // target.cu: Morton order of a point set (perm: sorted position -> original index, sorted: the
 // points in that order, packed xyz); n >= 1
 cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* sorted, cudaStream_t s, int* nlaunch);
@@ -154,7 +171,7 @@ cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* 
 // target.cu: stable LSD radix sort of (u64 key, u32 value) pairs by key bits [0, bits)
 size_t radix_sort_scratch_bytes(int n);
 cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long long* k1, uint32_t* v1, int n,
-                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt);
+                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt, bool pdl = false);
 
 // grid.cu: the uniform grid of a target (after its BVH build; quant = bbox min, qmax = bbox max
 // written by the build); allocates from the pool into *mem (owned by the target afterwards)
@@ -163,7 +180,8 @@ cudaError_t grid_build(const float* pts, int n, const float4* quant, const float
 
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);
-int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s);
+// (len <= 32,768, a multiple of 4: one launch of one block; pdl: programmatic dependent launches)
+int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s, bool pdl = false);
 
 }  // namespace cil
 

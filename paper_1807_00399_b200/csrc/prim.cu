@@ -39,6 +39,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
 }
 
 __global__ void tile_sum_kernel(const uint32_t* __restrict__ a, int64_t len, uint32_t* __restrict__ tsum) {
+    pdl_entry();
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     uint32_t s = 0;
 #pragma unroll
@@ -53,6 +54,7 @@ __global__ void tile_sum_kernel(const uint32_t* __restrict__ a, int64_t len, uin
 
 // exclusive scan of tsum[0..nt) in place, by one block (chunks of 256 with carry)
 __global__ void tile_prefix_kernel(uint32_t* __restrict__ tsum, int nt) {
+    pdl_entry();
     uint32_t carry = 0;
     for (int b = 0; b < nt; b += kScanThreads) {
         const int i = b + threadIdx.x;
@@ -65,6 +67,7 @@ __global__ void tile_prefix_kernel(uint32_t* __restrict__ tsum, int nt) {
 }
 
 __global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const uint32_t* __restrict__ tsum) {
+    pdl_entry();
     // each thread owns kScanItems consecutive elements of the tile
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems];
@@ -82,18 +85,73 @@ __global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const ui
     }
 }
 
+// Short arrays (the digit x tile tables of small sorts): the whole exclusive scan by one block of
+// 1024 threads, each owning a run of consecutive uint4 quads -- one launch instead of three.
+constexpr int kSmallScanThreads = 1024;
+constexpr int kSmallScanQuads = 8;                                         // per thread at most (loads issued together)
+constexpr int64_t kSmallScanMax = (int64_t)kSmallScanThreads * kSmallScanQuads * 4;   // 32,768
+
+template <int kSmallScanQuads>
+__global__ void __launch_bounds__(kSmallScanThreads)
+scan_small_kernel(uint32_t* a, int nquads) {
+    pdl_entry();
+    __shared__ uint32_t warp_tot[kSmallScanThreads / 32];
+    const int q0 = threadIdx.x * kSmallScanQuads;
+    uint4* a4 = reinterpret_cast<uint4*>(a);
+    uint4 v[kSmallScanQuads];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kSmallScanQuads; ++k) v[k] = q0 + k < nquads ? a4[q0 + k] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int k = 0; k < kSmallScanQuads; ++k) s += v[k].x + v[k].y + v[k].z + v[k].w;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;
+    }
+    __syncthreads();
+    uint32_t run = (w > 0 ? warp_tot[w - 1] : 0u) + x - s;
+#pragma unroll
+    for (int k = 0; k < kSmallScanQuads; ++k) {
+        uint4 o;
+        o.x = run; run += v[k].x;
+        o.y = run; run += v[k].y;
+        o.z = run; run += v[k].z;
+        o.w = run; run += v[k].w;
+        if (q0 + k < nquads) a4[q0 + k] = o;
+    }
+}
+
 }  // namespace
 
 size_t scan_temp_bytes(int64_t len) {
     return align_up((size_t)((len + kScanTile - 1) / kScanTile) * 4, 256);
 }
 
-int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s) {
+int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s, bool pdl) {
+    if (len <= kSmallScanMax && len % 4 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0) {
+        if (len <= kSmallScanMax / 2) launch_k(pdl, scan_small_kernel<kSmallScanQuads / 2>, 1, kSmallScanThreads, s, a, (int)(len / 4));
+        else launch_k(pdl, scan_small_kernel<kSmallScanQuads>, 1, kSmallScanThreads, s, a, (int)(len / 4));
+        return 1;
+    }
     const int nt = (int)((len + kScanTile - 1) / kScanTile);
     uint32_t* tsum = (uint32_t*)temp;
-    tile_sum_kernel<<<nt, kScanThreads, 0, s>>>(a, len, tsum);
-    tile_prefix_kernel<<<1, kScanThreads, 0, s>>>(tsum, nt);
-    tile_scan_kernel<<<nt, kScanThreads, 0, s>>>(a, len, tsum);
+    launch_k(pdl, tile_sum_kernel, nt, kScanThreads, s, (const uint32_t*)a, len, tsum);
+    launch_k(pdl, tile_prefix_kernel, 1, kScanThreads, s, tsum, nt);
+    launch_k(pdl, tile_scan_kernel, nt, kScanThreads, s, a, len, (const uint32_t*)tsum);
     return 3;
 }
 

@@ -27,6 +27,7 @@ constexpr int kThreads = 256;
 
 // ------------------------------------------------------------------ bbox
 __global__ void bbox_partial_kernel(const float* __restrict__ p, int n, float* __restrict__ part) {
+    pdl_entry();
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
 #pragma unroll
@@ -60,6 +61,7 @@ __global__ void bbox_partial_kernel(const float* __restrict__ p, int n, float* _
 
 // quant = (min.x, min.y, min.z, cells per unit); one block of kThreads
 __global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, float4* __restrict__ quant) {
+    pdl_entry();
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (int b = threadIdx.x; b < nblk; b += blockDim.x)
         for (int a = 0; a < 3; ++a) {
@@ -89,6 +91,7 @@ __global__ void bbox_final_kernel(const float* __restrict__ part, int nblk, floa
 
 __global__ void morton_kernel(const float* __restrict__ p, int n, const float4* __restrict__ quant,
                               unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_entry();
     const float4 Q = *quant;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         keys[i] = morton_of(Q, p[3 * (size_t)i], p[3 * (size_t)i + 1], p[3 * (size_t)i + 2]);
@@ -101,18 +104,44 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortWarps = kThreads / 32;
 constexpr int kItemsPerWarp = 512;                       // 16 rounds of 32
-constexpr int kTile = kSortWarps * kItemsPerWarp;         // 4096 keys per block
+// Small inputs are launch- and latency-bound (a 65,536-key pass at 4096 keys per block is 16
+// blocks of sequential rounds): their tile shrinks (down to one round per warp) until the pass
+// has up to kSmallBlocks blocks, which also keeps the digit x tile table within the one-block scan.
+#ifndef CIL_SMALL_TILES
+#define CIL_SMALL_TILES 1
+#endif
+#ifndef CIL_SMALL_BLOCKS
+#define CIL_SMALL_BLOCKS 64
+#endif
+constexpr int kSmallBlocks = CIL_SMALL_BLOCKS;       // 64 x 256 digits = the one-block scan's 16,384
+// items per warp of a sort over n keys (32 .. 512, a power of two)
+inline int sort_ipw(int n) {
+    int ipw = kItemsPerWarp;
+#if CIL_SMALL_TILES
+    while (ipw > 32 && ((int64_t)n + (kSortWarps * ipw / 2) - 1) / (kSortWarps * ipw / 2) <= kSmallBlocks) ipw >>= 1;
+#endif
+    return ipw;
+}
+inline int sort_blocks(int n) { const int tile = kSortWarps * sort_ipw(n); return std::max(1, (n + tile - 1) / tile); }
+// programmatic dependent launch for the build / ordering pipelines of inputs up to this size
+// (dozens of short kernels: launch gaps dominate; at 2M points it measured slower)
+#ifndef CIL_PDL_MAX_N
+#define CIL_PDL_MAX_N (1 << 15)
+#endif
+inline bool pipeline_pdl(int64_t n) { return n <= (int64_t)CIL_PDL_MAX_N; }
 
 __device__ __forceinline__ int digit_of(unsigned long long k, int shift) { return (int)((k >> shift) & (kRadix - 1)); }
 
 // hist[d * nblk + b] = number of keys with digit d in tile b
 __global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, int n, int shift,
-                                  uint32_t* __restrict__ hist, int nblk) {
+                                  uint32_t* __restrict__ hist, int nblk, int ipw) {
+    pdl_entry();
     __shared__ uint32_t h[kRadix];
     for (int d = threadIdx.x; d < kRadix; d += blockDim.x) h[d] = 0;
     __syncthreads();
-    const int base = blockIdx.x * kTile;
-    for (int i = threadIdx.x; i < kTile; i += blockDim.x) {
+    const int tile = kSortWarps * ipw;
+    const int base = blockIdx.x * tile;
+    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
         int g = base + i;
         if (g < n) atomicAdd(&h[digit_of(keys[g], shift)], 1u);
     }
@@ -120,18 +149,19 @@ __global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, i
     for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(size_t)d * nblk + blockIdx.x] = h[d];
 }
 
-// stable scatter: within a tile, warp w owns keys [w*512, (w+1)*512) processed in rounds of 32
+// stable scatter: within a tile, warp w owns keys [w*ipw, (w+1)*ipw) processed in rounds of 32
 __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin,
                                      unsigned long long* __restrict__ kout, uint32_t* __restrict__ vout,
-                                     int n, int shift, const uint32_t* __restrict__ offs, int nblk) {
+                                     int n, int shift, const uint32_t* __restrict__ offs, int nblk, int ipw) {
+    pdl_entry();
     __shared__ uint32_t cnt[kSortWarps][kRadix];   // per-warp digit counts, then offsets
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int d = l; d < kRadix; d += 32) cnt[w][d] = 0;
     __syncwarp();
-    const int wbase = blockIdx.x * kTile + w * kItemsPerWarp;
+    const int wbase = blockIdx.x * kSortWarps * ipw + w * ipw;
     const unsigned lt_mask = (1u << l) - 1u;
     // pass 1: per-warp digit histogram
-    for (int r = 0; r < kItemsPerWarp; r += 32) {
+    for (int r = 0; r < ipw; r += 32) {
         int g = wbase + r + l;
         bool ok = g < n;
         int d = ok ? digit_of(kin[g], shift) : -1;
@@ -151,7 +181,7 @@ __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin,
     }
     __syncthreads();
     // pass 2: scatter in position order
-    for (int r = 0; r < kItemsPerWarp; r += 32) {
+    for (int r = 0; r < ipw; r += 32) {
         int g = wbase + r + l;
         bool ok = g < n;
         unsigned long long k = ok ? kin[g] : 0ull;
@@ -174,6 +204,7 @@ __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin,
 __global__ void gather_kernel(const float* __restrict__ p, const float* __restrict__ nrm, int n,
                               const uint32_t* __restrict__ perm, float4* __restrict__ spts,
                               float4* __restrict__ opts, float4* __restrict__ onrm) {
+    pdl_entry();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t o = perm[i];
         const float x = p[3 * (size_t)o], y = p[3 * (size_t)o + 1], z = p[3 * (size_t)o + 2];
@@ -185,6 +216,7 @@ __global__ void gather_kernel(const float* __restrict__ p, const float* __restri
 
 __global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, int l_pad, float4* __restrict__ box,
                                 int n_leaves, float4* __restrict__ lbox) {
+    pdl_entry();
     for (int leaf = blockIdx.x * blockDim.x + threadIdx.x; leaf < l_pad; leaf += gridDim.x * blockDim.x) {
         float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f);
         float4 hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
@@ -206,6 +238,7 @@ __global__ void leaf_box_kernel(const float4* __restrict__ pts, int n, int B, in
 
 // SoA leaf blocks: leaf L holds rows x[B], y[B], z[B], idx[B]; padding slots get +inf / ~0
 __global__ void leaf_soa_kernel(const float4* __restrict__ pts, int n, int B, int64_t n_leaves, float* __restrict__ soa) {
+    pdl_entry();
     const int64_t total = n_leaves * B;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t leaf = g / B;
@@ -222,6 +255,7 @@ __global__ void leaf_soa_kernel(const float4* __restrict__ pts, int n, int B, in
 // cell_first[c] = first sorted index whose key >> shift >= c, for c in [0, ncell] (binary search)
 __global__ void cell_first_kernel(const unsigned long long* __restrict__ keys, int n, int shift, uint32_t ncell,
                                   uint32_t* __restrict__ cell_first) {
+    pdl_entry();
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= (int64_t)ncell;
          c += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = (unsigned long long)c << shift;
@@ -238,6 +272,7 @@ __global__ void cell_first_kernel(const unsigned long long* __restrict__ keys, i
 // of the current bottom level up `lv` levels, through shared memory.
 constexpr int kPassNodes = 256;
 __global__ void tree_pass_kernel(float4* __restrict__ box, int first, int lv) {
+    pdl_entry();
     __shared__ float4 slo[kPassNodes], shi[kPassNodes];
     const int t = threadIdx.x;
     const int width = min(kPassNodes, first);          // nodes per block at the bottom level
@@ -273,6 +308,7 @@ inline int grid_for(int64_t work, int threads = kThreads) {
 // src_sorted[k] = src[perm[k]] (packed xyz)
 __global__ void gather_xyz_kernel(const float* __restrict__ p, const uint32_t* __restrict__ perm, int n,
                                   float* __restrict__ out) {
+    pdl_entry();
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const size_t o = perm[k];
         out[3 * (size_t)k] = p[3 * o];
@@ -306,6 +342,7 @@ __device__ __forceinline__ float packet_diag(const float* p, int base, int n) {
 __global__ void __launch_bounds__(kThreads)
 order_choice_kernel(const float* __restrict__ a, const float* __restrict__ b, int n, double* __restrict__ part,
                     unsigned* __restrict__ ticket, int* __restrict__ keep_caller) {
+    pdl_entry();
     __shared__ double sa[kThreads / 32], sb[kThreads / 32];
     __shared__ int last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -339,6 +376,7 @@ order_choice_kernel(const float* __restrict__ a, const float* __restrict__ b, in
 
 __global__ void apply_order_kernel(const float* __restrict__ p, int n, const int* __restrict__ keep_caller,
                                    uint32_t* __restrict__ perm, float* __restrict__ sorted) {
+    pdl_entry();
     if (!*keep_caller) return;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         perm[k] = (uint32_t)k;
@@ -354,21 +392,22 @@ __global__ void apply_order_kernel(const float* __restrict__ p, int n, const int
 // ping-ponging between (k0, v0) and (k1, v1); *in_alt = true when the result ends in (k1, v1).
 // scratch: radix_sort_scratch_bytes(n) bytes of device memory.
 size_t radix_sort_scratch_bytes(int n) {
-    const int nblk = std::max(1, (n + kTile - 1) / kTile);
+    const int nblk = sort_blocks(n);
     return align_up((size_t)kRadix * nblk * 4, 256) + scan_temp_bytes((int64_t)kRadix * nblk);
 }
 
 cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long long* k1, uint32_t* v1, int n,
-                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt) {
-    const int nblk = std::max(1, (n + kTile - 1) / kTile);
+                             int bits, void* scratch, cudaStream_t s, int* nlaunch, bool* in_alt, bool pdl) {
+    const int nblk = sort_blocks(n), ipw = sort_ipw(n);
     uint32_t* hist = (uint32_t*)scratch;
     void* scan_tmp = (char*)scratch + align_up((size_t)kRadix * nblk * 4, 256);
     int nl = 0;
     bool alt = false;
     for (int shift = 0; shift < bits; shift += kRadixBits) {
-        radix_hist_kernel<<<nblk, kThreads, 0, s>>>(k0, n, shift, hist, nblk);
-        nl += 2 + scan_exclusive_u32(hist, (int64_t)kRadix * nblk, scan_tmp, s);
-        radix_scatter_kernel<<<nblk, kThreads, 0, s>>>(k0, v0, k1, v1, n, shift, hist, nblk);
+        launch_k(pdl, radix_hist_kernel, nblk, kThreads, s, (const unsigned long long*)k0, n, shift, hist, nblk, ipw);
+        nl += 2 + scan_exclusive_u32(hist, (int64_t)kRadix * nblk, scan_tmp, s, pdl);
+        launch_k(pdl, radix_scatter_kernel, nblk, kThreads, s, (const unsigned long long*)k0, (const uint32_t*)v0, k1, v1, n, shift,
+                 (const uint32_t*)hist, nblk, ipw);
         std::swap(k0, k1);
         std::swap(v0, v1);
         alt = !alt;
@@ -385,7 +424,8 @@ cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long
 // packets are at least as compact (decided on the device, no host synchronisation).  Scratch
 // from the library pool, stream-ordered.
 cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* sorted, cudaStream_t s, int* nlaunch) {
-    const int nblk_sort = (n + kTile - 1) / kTile;
+    const int nblk_sort = sort_blocks(n), ipw = sort_ipw(n);
+    const bool pdl = pipeline_pdl(n);
     const int nblk_bbox = grid_for(n);
     const size_t s_keys = align_up((size_t)n * 8, 256), s_vals = align_up((size_t)n * 4, 256);
     const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
@@ -408,24 +448,25 @@ cudaError_t morton_order_points(const float* pts, int n, uint32_t* perm, float* 
     int* keep = (int*)(cticket + 1);
     uint32_t* v0 = perm;                       // the values ping-pong between perm and v1
     int nl = 0;
-    bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, n, bbp);
-    bbox_final_kernel<<<1, kThreads, 0, s>>>(bbp, nblk_bbox, quant);
-    morton_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, n, quant, k0, v0);
+    launch_k(pdl, bbox_partial_kernel, nblk_bbox, kThreads, s, pts, n, bbp);
+    launch_k(pdl, bbox_final_kernel, 1, kThreads, s, (const float*)bbp, nblk_bbox, quant);
+    launch_k(pdl, morton_kernel, grid_for(n), kThreads, s, pts, n, (const float4*)quant, k0, v0);
     nl += 3;
     for (int shift = 3 * kMortonBits - 32; shift < 3 * kMortonBits; shift += kRadixBits) {
-        radix_hist_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, n, shift, hist, nblk_sort);
-        nl += 2 + scan_exclusive_u32(hist, (int64_t)kRadix * nblk_sort, scan_tmp, s);
-        radix_scatter_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, v0, k1, v1, n, shift, hist, nblk_sort);
+        launch_k(pdl, radix_hist_kernel, nblk_sort, kThreads, s, (const unsigned long long*)k0, n, shift, hist, nblk_sort, ipw);
+        nl += 2 + scan_exclusive_u32(hist, (int64_t)kRadix * nblk_sort, scan_tmp, s, pdl);
+        launch_k(pdl, radix_scatter_kernel, nblk_sort, kThreads, s, (const unsigned long long*)k0, (const uint32_t*)v0, k1, v1, n,
+                 shift, (const uint32_t*)hist, nblk_sort, ipw);
         std::swap(k0, k1);
         std::swap(v0, v1);
     }
     // 4 passes: the sorted values are back in perm
-    gather_xyz_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, perm, n, sorted);
+    launch_k(pdl, gather_xyz_kernel, grid_for(n), kThreads, s, pts, (const uint32_t*)perm, n, sorted);
     // keep the caller's order when it is at least as coherent (scan-ordered LiDAR / depth frames)
     if (!(debug_flags() & 32u)) {                 // diagnostics bit 5: always the Morton order
         cudaMemsetAsync(cticket, 0, 8, s);
-        order_choice_kernel<<<kExtBlocks, kThreads, 0, s>>>(pts, sorted, n, cpart, cticket, keep);
-        apply_order_kernel<<<grid_for(n), kThreads, 0, s>>>(pts, n, keep, perm, sorted);
+        launch_k(pdl, order_choice_kernel, kExtBlocks, kThreads, s, pts, (const float*)sorted, n, cpart, cticket, keep);
+        launch_k(pdl, apply_order_kernel, grid_for(n), kThreads, s, pts, n, (const int*)keep, perm, sorted);
         nl += 3;
     }
     e = cudaGetLastError();
@@ -506,7 +547,8 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     float4* d_lbox = (float4*)(base + b_pts + b_nrm + b_box + b_keys + b_cell + b_quant + b_soa);
 
     // scratch: keys x2 (8N), vals x2 (4N), hist (256 * nblk), bbox partials
-    const int nblk_sort = (N + kTile - 1) / kTile;
+    const int nblk_sort = sort_blocks(N), ipw = sort_ipw(N);
+    const bool pdl = pipeline_pdl(N);
     const int nblk_bbox = grid_for(N);
     const size_t s_keys = align_up((size_t)N * 8, 256), s_vals = align_up((size_t)N * 4, 256);
     const size_t s_hist = align_up((size_t)kRadix * nblk_sort * 4, 256);
@@ -529,26 +571,27 @@ CIL_API cil_status cil_target_build(const float* pts, const float* normals, int6
     int nlaunch = 0;
 
     prof_begin(kProfBuild, s);
-    bbox_partial_kernel<<<nblk_bbox, kThreads, 0, s>>>(pts, N, bbp);
-    bbox_final_kernel<<<1, kThreads, 0, s>>>(bbp, nblk_bbox, d_quant);
-    morton_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, N, d_quant, k0, v0);
+    launch_k(pdl, bbox_partial_kernel, nblk_bbox, kThreads, s, pts, N, bbp);
+    launch_k(pdl, bbox_final_kernel, 1, kThreads, s, (const float*)bbp, nblk_bbox, d_quant);
+    launch_k(pdl, morton_kernel, grid_for(N), kThreads, s, pts, N, (const float4*)d_quant, k0, v0);
     for (int shift = 0; shift < 3 * kMortonBits; shift += kRadixBits) {
-        radix_hist_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, N, shift, hist, nblk_sort);
-        nlaunch += scan_exclusive_u32(hist, (int64_t)kRadix * nblk_sort, scan_tmp, s);
-        radix_scatter_kernel<<<nblk_sort, kThreads, 0, s>>>(k0, v0, k1, v1, N, shift, hist, nblk_sort);
+        launch_k(pdl, radix_hist_kernel, nblk_sort, kThreads, s, (const unsigned long long*)k0, N, shift, hist, nblk_sort, ipw);
+        nlaunch += scan_exclusive_u32(hist, (int64_t)kRadix * nblk_sort, scan_tmp, s, pdl);
+        launch_k(pdl, radix_scatter_kernel, nblk_sort, kThreads, s, (const unsigned long long*)k0, (const uint32_t*)v0, k1, v1, N,
+                 shift, (const uint32_t*)hist, nblk_sort, ipw);
         std::swap(k0, k1);
         std::swap(v0, v1);
     }
-    gather_kernel<<<grid_for(N), kThreads, 0, s>>>(pts, normals, N, v0, spts, d_pts, d_nrm);
+    launch_k(pdl, gather_kernel, grid_for(N), kThreads, s, pts, normals, N, v0, spts, d_pts, d_nrm);
     cudaMemcpyAsync(d_keys, k0, (size_t)N * 8, cudaMemcpyDeviceToDevice, s);
-    cell_first_kernel<<<grid_for(ncell + 1), kThreads, 0, s>>>(k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
-    leaf_box_kernel<<<grid_for(l_pad), kThreads, 0, s>>>(spts, N, B, (int)l_pad, d_box, (int)n_leaves, d_lbox);
-    leaf_soa_kernel<<<grid_for(n_leaves * B), kThreads, 0, s>>>(spts, N, B, n_leaves, d_soa);
+    launch_k(pdl, cell_first_kernel, grid_for(ncell + 1), kThreads, s, k0, N, 3 * kMortonBits - coarse_bits, (uint32_t)ncell, d_cell);
+    launch_k(pdl, leaf_box_kernel, grid_for(l_pad), kThreads, s, spts, N, B, (int)l_pad, d_box, (int)n_leaves, d_lbox);
+    launch_k(pdl, leaf_soa_kernel, grid_for(n_leaves * B), kThreads, s, spts, N, B, n_leaves, d_soa);
     int tree_passes = 0;
     for (int first = (int)l_pad, rem = levels; rem > 0; ++tree_passes) {
         const int lv = std::min(rem, 8);
         const int width = std::min(kPassNodes, first);
-        tree_pass_kernel<<<first / width, kPassNodes, 0, s>>>(d_box, first, lv);
+        launch_k(pdl, tree_pass_kernel, first / width, kPassNodes, s, d_box, first, lv);
         first >>= lv;
         rem -= lv;
     }

@@ -323,7 +323,10 @@ __global__ void gather_xyz_kernel(const float* __restrict__ p, const uint32_t* _
 // unless the Morton order is clearly more coherent.  Deterministic run to run.  (Measured:
 // scan-ordered LiDAR and depth frames search faster in their scan order even though Morton
 // packets have slightly shorter paths; random-order samples gain up to 10x from the sort.)
-constexpr int kExtBlocks = 256;
+#ifndef CIL_EXT_BLOCKS
+#define CIL_EXT_BLOCKS 592     // (4 per SM; 256 measured 0.2 % slower on the C4 run, 1184 equal)
+#endif
+constexpr int kExtBlocks = CIL_EXT_BLOCKS;
 // path length of a 32-point packet, sum |p_{i+1} - p_i| (rotation invariant): ~ the arc length
 // for a scan line, much more for a packet that zigzags between scan lines or jumps around
 __device__ __forceinline__ float packet_diag(const float* p, int base, int n) {
@@ -363,10 +366,18 @@ order_choice_kernel(const float* __restrict__ a, const float* __restrict__ b, in
         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last || threadIdx.x != 0) return;
+    if (!last || threadIdx.x >= 32) return;
     __threadfence();
+    // the last block's first warp adds the partials in a fixed order (lane-strided, then a
+    // butterfly: every lane ends with the same bits)
     double ta = 0.0, tb = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) { ta += __ldcg(part + 2 * k); tb += __ldcg(part + 2 * k + 1); }
+    for (int k = lane; k < (int)gridDim.x; k += 32) { ta += __ldcg(part + 2 * k); tb += __ldcg(part + 2 * k + 1); }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ta += __shfl_xor_sync(0xffffffffu, ta, o);
+        tb += __shfl_xor_sync(0xffffffffu, tb, o);
+    }
+    if (lane != 0) return;
     // keep the caller's order unless its packets are clearly less coherent: geometric-mean path
     // length more than 4x the Morton order's (random-order samples: C5 patch-major, C1)
     const double npk_d = (double)((n + 31) / 32);

@@ -83,6 +83,19 @@ def test_nn_small_ragged(cil, n, m, leaf, index):
     assert info.n == n and info.leaf_size == leaf and info.n_leaves == (n + leaf - 1) // leaf
 
 
+@pytest.mark.parametrize("n", [257, 2049, 8193, 16385, 32769, 131073])
+def test_nn_build_sort_tile_regimes(cil, n):
+    """index builds on both sides of every small-input sort-tile size and scan path (and of the
+    programmatic-dependent-launch threshold, 32,768 points): every query against the oracle"""
+    rng = np.random.default_rng(n)
+    T = rng.standard_normal((n, 3)).astype(np.float32)
+    Q = (rng.standard_normal((4001, 3)) * 1.1).astype(np.float32)
+    t = cil.cil_target_build(dev(T), None)
+    gi, gd = cil.cil_nn_query(t, dev(Q))
+    o_idx, o_d2 = oracle.knn(T, Q.astype(np.float64), k=2)
+    check_nn(T, Q.astype(np.float64), gi.cpu().numpy(), gd.cpu().numpy(), o_idx, o_d2)
+
+
 @pytest.mark.parametrize("index", INDEXES)
 def test_nn_ties_lowest_original_index(cil, index):
     """R1: exact ties (duplicated integer grid points, cube centres) -> lowest original index."""

@@ -46,6 +46,17 @@ def test_voxel_random_ragged(cil, n, h):
     check(cil, p, h, (0.013, -0.2, 0.3), nrm)
 
 
+@pytest.mark.parametrize("n", [255, 257, 2049, 8193, 16384, 16385, 32769, 65537, 131073, 262145, 300001])
+def test_voxel_sort_tile_regimes(cil, n):
+    """sizes on both sides of every sort-tile size (256 ... 4096 keys per CTA, up to 64 CTAs per
+    pass for small inputs) and of the one-block / three-kernel scan of the digit x tile table:
+    the stable radix sort decides the bins' input order, so the means are bit-exact only if it
+    is right"""
+    rng = np.random.default_rng(n)
+    p = (rng.random((n, 3)) * 4.0 - 2.0).astype(np.float32)
+    check(cil, p, 0.03, (0.0, 0.1, -0.2))
+
+
 def test_voxel_c3_one_centimetre(cil):
     """the paper's ICP preprocessing: 1 cm voxels on the C3 depth frame"""
     w = W.c3()

@@ -461,7 +461,9 @@ def _check_normals(cil, pts, k, view, min_gap=1e-3):
     """cil_estimate_normals vs oracle.pca_normals: where the k-NN set is unambiguous (the k-th
     and (k+1)-th fp64 distances differ by > 1e-6 relative) and the smallest eigenvalue is
     separated (relative eigengap > min_gap), the normals agree to 1e-6 rad and the curvature to
-    1e-5 relative; everywhere the GPU normal is a unit vector facing the viewpoint."""
+    1e-5 relative; wherever the k-NN set is unambiguous the normal's Rayleigh quotient equals the
+    smallest eigenvalue and the curvature agrees; everywhere the GPU normal is a unit vector
+    facing the viewpoint."""
     t = cil.cil_target_build(dev(pts), None)
     g, gc = cil.cil_estimate_normals(t, k, view, want_curvature=True)
     g, gc = g.cpu().numpy().astype(np.float64), gc.cpu().numpy().astype(np.float64)
@@ -484,6 +486,15 @@ def _check_normals(cil, pts, k, view, min_gap=1e-3):
     assert ang.max() <= 1e-6, ang.max()
     assert ((g[ok] * o[ok]).sum(1) > 0).all()                     # same orientation
     np.testing.assert_allclose(gc[ok], oc[ok].astype(np.float64), rtol=1e-5, atol=1e-9)
+    # every point with an unambiguous k-NN set, whatever its eigengap: the direction is
+    # ill-conditioned where the two smallest eigenvalues meet, but the Rayleigh quotient of the
+    # GPU normal on the oracle-side covariance is not -- it must sit at the smallest eigenvalue
+    # (within 1e-5 of the spectrum's scale), and so must the curvature
+    gu = g[clear] / np.linalg.norm(g[clear], axis=1, keepdims=True)
+    ray = np.einsum("ni,nij,nj->n", gu, Cv[clear], gu)
+    assert (ray <= ev[clear, 0] + 1e-5 * np.maximum(ev[clear, 2], 1e-300)).all(), \
+        float((ray - ev[clear, 0]).max())
+    np.testing.assert_allclose(gc[clear], oc[clear].astype(np.float64), rtol=1e-5, atol=1e-9)
     np.testing.assert_allclose(np.linalg.norm(g, axis=1), 1.0, atol=1e-6)
     assert (((np.asarray(view) - pts.astype(np.float64)) * g).sum(1) >= -1e-6).all()
     return ok.mean()

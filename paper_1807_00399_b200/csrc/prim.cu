@@ -10,6 +10,10 @@ namespace {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;                          // per thread
 constexpr int kScanTile = kScanThreads * kScanItems;    // 4096 per block
+#ifndef CIL_SCAN_FUSED_PREFIX
+#define CIL_SCAN_FUSED_PREFIX 1
+#endif
+constexpr int kFusedPrefixTiles = 2048;                 // up to this many tiles every block sums its predecessors itself
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
     __shared__ uint32_t warp_tot[kScanThreads / 32];
@@ -66,7 +70,9 @@ __global__ void tile_prefix_kernel(uint32_t* __restrict__ tsum, int nt) {
     }
 }
 
-__global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const uint32_t* __restrict__ tsum) {
+// raw = true: tsum holds the tiles' sums (no tile_prefix_kernel ran): the block adds up the sums
+// of the tiles before it (a few hundred values: cheaper than a third launch)
+__global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const uint32_t* __restrict__ tsum, bool raw) {
     pdl_entry();
     // each thread owns kScanItems consecutive elements of the tile
     const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
@@ -77,7 +83,17 @@ __global__ void tile_scan_kernel(uint32_t* __restrict__ a, int64_t len, const ui
         v[k] = base + k < len ? a[base + k] : 0u;
         s += v[k];
     }
-    uint32_t run = tsum[blockIdx.x] + block_exclusive_scan(s, nullptr);
+    uint32_t tile_base;
+    if (raw) {
+        uint32_t p = 0;
+        for (int b = threadIdx.x; b < (int)blockIdx.x; b += kScanThreads) p += tsum[b];
+        uint32_t tot;
+        block_exclusive_scan(p, &tot);
+        tile_base = tot;
+    } else {
+        tile_base = tsum[blockIdx.x];
+    }
+    uint32_t run = tile_base + block_exclusive_scan(s, nullptr);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         if (base + k < len) a[base + k] = run;
@@ -150,9 +166,10 @@ int scan_exclusive_u32(uint32_t* a, int64_t len, void* temp, cudaStream_t s, boo
     const int nt = (int)((len + kScanTile - 1) / kScanTile);
     uint32_t* tsum = (uint32_t*)temp;
     launch_k(pdl, tile_sum_kernel, nt, kScanThreads, s, (const uint32_t*)a, len, tsum);
-    launch_k(pdl, tile_prefix_kernel, 1, kScanThreads, s, tsum, nt);
-    launch_k(pdl, tile_scan_kernel, nt, kScanThreads, s, a, len, (const uint32_t*)tsum);
-    return 3;
+    const bool raw = CIL_SCAN_FUSED_PREFIX && nt <= kFusedPrefixTiles;
+    if (!raw) launch_k(pdl, tile_prefix_kernel, 1, kScanThreads, s, tsum, nt);
+    launch_k(pdl, tile_scan_kernel, nt, kScanThreads, s, a, len, (const uint32_t*)tsum, raw);
+    return raw ? 2 : 3;
 }
 
 }  // namespace cil

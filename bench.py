@@ -404,8 +404,14 @@ def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
     s_copy = torch.cuda.Stream(device=dev)
 
     def step():
-        # target + normals first on the launching stream (the build needs them), the source on a
-        # second stream so that its copy overlaps the index build
+        if not args.split:
+            # the C-ABI host-buffer call: copies in (the source on the library's second stream,
+            # overlapping the index build), build, run, result out -- all inside libcil.so
+            r = cil.cil_icp_align_host(h_t, h_n, h_s, None, prm, leaf_size=args.leaf or 0)
+            assert r.status == 0, r.status
+            return
+        # split: target + normals first on the launching stream (the build needs them), the source
+        # on a second stream so that its copy overlaps the index build
         d_t.copy_(h_t, non_blocking=True)
         if d_n is not None:
             d_n.copy_(h_n, non_blocking=True)
@@ -444,7 +450,8 @@ def _e2e(args, w, iters, cil, dev, flush, rank, world, lo, hi):
     tmax, pairs = reduce_over_ranks(tot, float(hi - lo) * iters * args.steps, world, dev)
     h2d = h_t.numel() * 4 + (h_n.numel() * 4 if h_n is not None else 0) + h_s.numel() * 4
     return {"value": pairs / (tmax / 1e3), "unit": UNIT, "ms_per_step": tmax / args.steps,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(h_res.numel())}
+            "h2d_bytes_per_step": int(h2d) + (0 if args.split else 128), "d2h_bytes_per_step": int(h_res.numel()),
+            "call": "ShardRun (torch copies + C ABI)" if args.split else "cil_icp_align_host (C ABI, pinned host buffers)"}
 
 
 # ---------------------------------------------------------------------------- oracle arm

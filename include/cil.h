@@ -208,6 +208,23 @@ cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const d
                        const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
                        double* iter_log, cil_stream_t stream);
 
+/* The whole registration of one frame pair from HOST buffers (the end-to-end call: what the
+   paper's benchmark times per pair, "Total registration times"): copies the
+   target (and its normals), the source and the initial pose to the device, builds the index,
+   runs cil_icp_run and copies the result back.  EVERY pointer is a HOST pointer here:
+   target / normals fp32 [n*3] (normals NULL allowed for point-to-point), source fp32 [m*3],
+   pose_init fp64[16] row-major (NULL = identity), result: host cil_icp_result.  Page-locked
+   (pinned) host buffers make the copies asynchronous -- the source copy then runs on an
+   internal second stream and overlaps the index build; pageable buffers work but are staged
+   by the driver.  index: cil_index_params or NULL.  Device memory (inputs, workspace, result)
+   comes from the library's stream-ordered pool and is released before returning.
+   SYNCHRONOUS on `stream`: returns after the result is in *result (it synchronises that
+   stream, not the device).  Errors as cil_target_build / cil_icp_run; on an error *result is
+   not written.  Same kernels and bitwise the same result as the device-pointer calls. */
+cil_status cil_icp_align_host(const float* target, const float* normals, int64_t n, const float* source, int64_t m,
+                              const double* pose_init, const cil_icp_params* params, const cil_index_params* index,
+                              cil_icp_result* result, cil_stream_t stream);
+
 /* Surface normals of the TARGET points by PCA over their k nearest neighbours (SURVEY.md
    8(f) NEXT-3; "normal estimation", PAPER.md:172-176 10-NN normals oriented
    towards the viewpoint): for every target point p the exact k nearest targets (p itself

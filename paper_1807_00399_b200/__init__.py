@@ -50,7 +50,7 @@ EXPORTED = ["cil_target_build", "cil_target_free", "cil_target_get_info", "cil_n
             "cil_debug_set_flags", "cil_debug_engine_trace", "cil_debug_set_cert_skin",
             "cil_proj_workspace_bytes", "cil_proj_iterate", "cil_proj_run", "cil_debug_timestamps",
             "cil_voxel_downsample", "cil_icp_shard_begin", "cil_icp_shard_accumulate", "cil_icp_shard_finish",
-            "cil_icp_shard_result"]
+            "cil_icp_shard_result", "cil_icp_align_host"]
 
 
 class cil_index_params(C.Structure):
@@ -115,6 +115,9 @@ _lib.cil_icp_iterate.restype = C.c_int
 _lib.cil_icp_iterate.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp, _vp, _vp]
 _lib.cil_icp_run.restype = C.c_int
 _lib.cil_icp_run.argtypes = [_vp, _vp, _i64, _vp, C.POINTER(cil_icp_params), _vp, _sz, _vp, _vp, _vp]
+_lib.cil_icp_align_host.restype = C.c_int
+_lib.cil_icp_align_host.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, C.POINTER(cil_icp_params), C.POINTER(cil_index_params),
+                                    C.POINTER(cil_icp_result), _vp]
 _lib.cil_proj_workspace_bytes.restype = _sz
 _lib.cil_proj_workspace_bytes.argtypes = [_i64, C.POINTER(cil_icp_params)]
 _lib.cil_proj_iterate.restype = C.c_int
@@ -410,6 +413,39 @@ def cil_icp_run(t: Target, src: torch.Tensor, pose_init: torch.Tensor, params: c
     _check(_lib.cil_icp_run(t.handle, _ptr(src), m, _ptr(pose_init), C.byref(params), _ptr(ws), ws.numel(),
                             _ptr(res), _ptr(iter_log), t.use(stream)), "cil_icp_run")
     return res, iter_log
+
+
+def _host_pts(t, name: str) -> torch.Tensor:
+    t = torch.as_tensor(t)
+    if t.is_cuda or t.dtype != torch.float32 or t.dim() != 2 or t.shape[1] != 3 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous HOST float32 array of shape [n, 3]")
+    return t
+
+
+def cil_icp_align_host(target, normals, source, pose_init=None, params: cil_icp_params | None = None,
+                       leaf_size: int = 0, index: str = "bvh", stream=None) -> "Result":
+    """One frame pair end to end from HOST buffers through the C ABI (cil_icp_align_host): the
+    copies in, the index build, the device-resident loop and the result copy all happen inside
+    the library call.  Inputs: CPU float32 [n, 3] tensors / arrays (pinned tensors make the
+    copies asynchronous), pose_init a CPU float64 [4, 4] or None (identity).  Synchronous."""
+    ht = _host_pts(target, "target")
+    hn = _host_pts(normals, "normals") if normals is not None else None
+    hs = _host_pts(source, "source")
+    if hn is not None and hn.shape != ht.shape:
+        raise ValueError("normals must match target")
+    hp = None
+    if pose_init is not None:
+        hp = torch.as_tensor(pose_init, dtype=torch.float64).contiguous()
+        if hp.is_cuda or hp.shape != (4, 4):
+            raise ValueError("pose_init must be a HOST float64 [4, 4]")
+    ip = cil_index_params()
+    ip.leaf_size = int(leaf_size)
+    ip.index_kind = {"bvh": CIL_INDEX_BVH, "grid": CIL_INDEX_GRID}[index]
+    r = cil_icp_result()
+    _check(_lib.cil_icp_align_host(_ptr(ht), _ptr(hn), ht.shape[0], _ptr(hs), hs.shape[0], _ptr(hp),
+                                   C.byref(params if params is not None else make_params()), C.byref(ip), C.byref(r),
+                                   _stream_ptr(stream)), "cil_icp_align_host")
+    return Result(np.array(r.pose).reshape(4, 4), r.rmse, r.n_corr, r.iterations, bool(r.converged), r.status)
 
 
 # ---------------------------------------------------------------- projective engine (NEXT-2)

@@ -95,6 +95,16 @@ def test_host_side_argument_errors(cil):
     assert L.cil_icp_iterate(None, None, 10, None, C.byref(p), None, 0, None, None, None, None, None) == \
         cil.CIL_ERR_INVALID_ARG
     assert L.cil_icp_run(None, None, 10, None, C.byref(p), None, 0, None, None, None) == cil.CIL_ERR_INVALID_ARG
+    # the host-buffer call: argument errors come back before any CUDA call
+    r = cil.cil_icp_result()
+    hp = C.c_void_p(4096)
+    assert L.cil_icp_align_host(hp, None, 10, hp, 10, None, C.byref(p), None, None, None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_align_host(hp, None, 10, hp, 10, None, None, None, C.byref(r), None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_align_host(hp, None, 0, hp, 10, None, C.byref(p), None, C.byref(r), None) == cil.CIL_ERR_EMPTY_TARGET
+    assert L.cil_icp_align_host(hp, None, -1, hp, 10, None, C.byref(p), None, C.byref(r), None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_align_host(hp, None, 10, hp, 2 ** 31, None, C.byref(p), None, C.byref(r), None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_align_host(None, None, 10, hp, 10, None, C.byref(p), None, C.byref(r), None) == cil.CIL_ERR_INVALID_ARG
+    assert L.cil_icp_align_host(hp, None, 10, None, 10, None, C.byref(p), None, C.byref(r), None) == cil.CIL_ERR_INVALID_ARG
     assert L.cil_target_free(None, None) == cil.CIL_OK
     assert L.cil_status_string(cil.CIL_ERR_DEGENERATE) == b"CIL_ERR_DEGENERATE"
 

@@ -515,6 +515,50 @@ def test_normals_c3_config(cil):
     assert frac > 0.95
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("metric", ["point_to_plane", "point_to_point"])
+def test_align_host_equals_device_path(cil, metric, pinned):
+    """cil_icp_align_host (HOST buffers in, result out, one C call) = cil_target_build +
+    cil_icp_run on device buffers, bit for bit; pinned and pageable inputs; a given initial pose
+    and the NULL (identity) one; against the oracle within the north_star tolerances"""
+    w = W.c4(metric, 16, 8000)
+    prm = cil.make_params(metric, 12, w.max_dist)
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    hold = (lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()) if pinned else \
+        (lambda a: torch.as_tensor(np.ascontiguousarray(a)))
+    for P0 in (None, w.gt_pose @ np.array([[1, 0, 0, 0.05], [0, 1, 0, -0.02], [0, 0, 1, 0.01], [0, 0, 0, 1.0]])):
+        d_p0 = dev(np.eye(4) if P0 is None else P0)
+        ref = cil.decode_result(cil.cil_icp_run(t, dev(w.source), d_p0, prm, want_log=False)[0])
+        got = cil.cil_icp_align_host(hold(w.target), hold(w.target_normals), hold(w.source), P0, prm)
+        assert got.status == ref.status == 0 and got.iterations == ref.iterations == 12
+        assert got.n_corr == ref.n_corr and got.rmse == ref.rmse
+        assert np.array_equal(got.pose, ref.pose)
+    o = oracle.icp_run(w.target, w.target_normals, w.source, metric, 12, w.max_dist)
+    got = cil.cil_icp_align_host(hold(w.target), hold(w.target_normals), hold(w.source), None, prm)
+    assert W.rot_angle(got.pose[:3, :3] @ o.pose[:3, :3].T) <= 1e-4
+    assert np.abs(got.pose[:3, 3] - o.pose[:3, 3]).max() <= 1e-5
+    t.free()
+
+
+def test_align_host_errors_and_edge_cases(cil):
+    """missing normals for point-to-plane -> CIL_ERR_NO_NORMALS (nothing leaks: the call can be
+    repeated); an empty source -> CIL_NO_CORRESPONDENCES on the device, identity pose; the small
+    brute-force path (C1) through the host call"""
+    w = W.c1()
+    prm = cil.make_params("point_to_plane", 5, w.max_dist)
+    for _ in range(3):
+        with pytest.raises(cil.CilError) as ei:
+            cil.cil_icp_align_host(w.target, None, w.source, None, prm)
+        assert ei.value.status == cil.CIL_ERR_NO_NORMALS
+    r = cil.cil_icp_align_host(w.target, w.target_normals, np.zeros((0, 3), np.float32), None, prm)
+    assert r.status == cil.CIL_NO_CORRESPONDENCES and np.array_equal(r.pose, np.eye(4))
+    t = cil.cil_target_build(dev(w.target), dev(w.target_normals))
+    ref = cil.decode_result(cil.cil_icp_run(t, dev(w.source), dev(np.eye(4)), prm, want_log=False)[0])
+    got = cil.cil_icp_align_host(w.target, w.target_normals, w.source, None, prm)
+    assert got.status == 0 and np.array_equal(got.pose, ref.pose) and got.n_corr == ref.n_corr
+    t.free()
+
+
 def test_run_empty_source(cil):
     """cil_icp_run with m = 0: CIL_NO_CORRESPONDENCES after one iteration, identity pose"""
     w = W.c1()

@@ -774,7 +774,7 @@ icp_select_kernel(const IterArgs a) {
 }
 
 // ---------------------------------------------------------------- K_nn
-constexpr int kNNThreads = 256;
+constexpr int kNNThreads = 32 * kEngineWarps;
 
 template <int B, bool CERT>
 struct IcpQueries {

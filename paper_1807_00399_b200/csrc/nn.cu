@@ -10,7 +10,10 @@
 namespace cil {
 namespace {
 
-constexpr int kNNThreads = 256;
+constexpr int kNNThreads = 32 * kEngineWarps;
+#ifndef CIL_NNQ_MINB
+#define CIL_NNQ_MINB 4
+#endif
 
 // Queries are processed in the order of perm (a counting sort by the target's coarse Morton
 // cell) so that the 32 queries of a warp packet are spatial neighbours; results are written
@@ -60,7 +63,7 @@ __global__ void qcell_scatter_kernel(const uint32_t* __restrict__ qcell, int m, 
 }
 
 template <int B>
-__global__ void __launch_bounds__(kNNThreads, 4)
+__global__ void __launch_bounds__(kNNThreads, CIL_NNQ_MINB)
 nn_query_kernel(TargetView T, NNQueries qs, int m, unsigned int* counter) {
     nn_packet_engine<B, false>(T, qs, m, counter);
 }

@@ -318,7 +318,10 @@ constexpr int kItemCap = 256;
 #endif
 constexpr int kDGroup = CIL_DGROUP;      // frontier leaves tested per step of phase D
 constexpr int kDirectLeaves = CIL_DIRECT_LEAVES;
-constexpr int kEngineWarps = 8;     // warps per block of the engine kernels (blockDim 256)
+#ifndef CIL_ENGINE_WARPS
+#define CIL_ENGINE_WARPS 8
+#endif
+constexpr int kEngineWarps = CIL_ENGINE_WARPS;     // warps per block of the engine kernels (blockDim 32 x this)
 
 // Independent per-lane exact DFS (nearest-child first, a subtree is entered iff its lower
 // bound is <= the lane's current threshold), for outlier lanes, overflowed packets and

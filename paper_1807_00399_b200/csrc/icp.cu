@@ -458,7 +458,10 @@ __device__ __forceinline__ float displacement_bound(const float* __restrict__ D,
 // K_sel writes, per packet of 32 consecutive source points, the mask of the points that need
 // a full search; K_nn then runs its packets in source order with only those lanes active, so
 // an uncertified remainder stays spatially coherent (a compacted list would scatter it).
-constexpr int kSelThreads = 256;
+#ifndef CIL_SEL_THREADS
+#define CIL_SEL_THREADS 128     // (6 CTAs per SM; 256: C4 run +2.7 %, 64: +2.4 %, 384: +4 %)
+#endif
+constexpr int kSelThreads = CIL_SEL_THREADS;
 #ifndef CIL_SEL_PREFETCH
 #define CIL_SEL_PREFETCH 1     // a queued record's candidate list prefetched at classification (C4 run -0.4 %)
 #endif
@@ -687,7 +690,7 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
 }
 
 #if CIL_SEL_PERSIST
-#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads, 3)
+#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads, 768 / kSelThreads)
 #else
 #define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads)
 #endif

@@ -690,7 +690,10 @@ __device__ __forceinline__ void evaluate_records(const IterArgs& a, const Pose34
 }
 
 #if CIL_SEL_PERSIST
-#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads, 768 / kSelThreads)
+#ifndef CIL_SEL_MINB
+#define CIL_SEL_MINB (768 / kSelThreads)
+#endif
+#define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads, CIL_SEL_MINB)
 #else
 #define CIL_SEL_BOUNDS __launch_bounds__(kSelThreads)
 #endif

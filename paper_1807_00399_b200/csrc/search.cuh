@@ -309,7 +309,10 @@ __device__ __forceinline__ int coarse_hint_leaf(const TargetView& T, const DF3& 
 #define CIL_DIRECT_LEAVES 512
 #endif
 constexpr int kFrontierCap = CIL_FRONTIER_CAP;
-constexpr int kItemCap = 256;
+#ifndef CIL_ITEM_CAP
+#define CIL_ITEM_CAP 256
+#endif
+constexpr int kItemCap = CIL_ITEM_CAP;
 #ifndef CIL_DGROUP
 #define CIL_DGROUP 2
 #endif

@@ -1,6 +1,6 @@
 // host.cu -- cil_icp_align_host: one frame pair end to end from HOST buffers (cil.h): H2D copies
-// (the source on a second stream, overlapping the index build), cil_target_build, cil_icp_run,
-// the result copied back.  Only plumbing around the device-pointer calls: no arithmetic here.
+// (the source and its ordering step on a second stream, overlapping the target's copy and index
+// build), cil_target_build, cil_icp_run, the result copied back.  Only plumbing around the device-pointer calls: no arithmetic here.
 #include "internal.cuh"
 
 #include <algorithm>
@@ -89,6 +89,10 @@ CIL_API cil_status cil_icp_align_host(const float* target, const float* normals,
         return fail("H2D source");
     if ((e = cudaMemcpyAsync(d_pose, pose_init ? pose_init : kIdentity, 128, cudaMemcpyHostToDevice, side->s)) != cudaSuccess)
         return fail("H2D pose");
+    // the run's source-order step depends only on the source: on the second stream too, under the
+    // target's copy and build (the small-problem path does not order its source)
+    const bool ordered = m > 0 && !icp_small_path_nm(n, m);
+    if (ordered && (e = icp_order_source(d_ws, d_s, m, side->s)) != cudaSuccess) return fail("source order");
     if ((e = cudaEventRecord(side->copied, side->s)) != cudaSuccess) return fail("cudaEventRecord");
     // target (+ normals) on the launching stream: the build needs them first
     if ((e = cudaMemcpyAsync(d_t, target, (size_t)n * 12, cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail("H2D target");
@@ -96,7 +100,9 @@ CIL_API cil_status cil_icp_align_host(const float* target, const float* normals,
         return fail("H2D normals");
     if ((rc = cil_target_build(d_t, d_n, n, index, stream, &t)) != CIL_OK) return fail("");
     if ((e = cudaStreamWaitEvent(s, side->copied, 0)) != cudaSuccess) return fail("cudaStreamWaitEvent");
-    if ((rc = cil_icp_run(t, d_s, m, d_pose, params, d_ws, ws_bytes, d_res, nullptr, stream)) != CIL_OK) return fail("");
+    rc = ordered ? icp_run_ordered(t, d_s, m, d_pose, params, d_ws, ws_bytes, d_res, stream)
+                 : cil_icp_run(t, d_s, m, d_pose, params, d_ws, ws_bytes, d_res, nullptr, stream);
+    if (rc != CIL_OK) return fail("");
     cil_icp_result tmp;
     if ((e = cudaMemcpyAsync(&tmp, d_res, sizeof(tmp), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail("D2H result");
     cil_target_free(t, stream);

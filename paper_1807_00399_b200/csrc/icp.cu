@@ -2180,9 +2180,15 @@ void run_args(IterArgs& a, const cil_target* t, const float* src, int64_t m, con
 }
 
 // sorted source + state initialisation of a run
-cil_status run_begin(IterArgs& a, const float* src, int64_t m, const double* pose_init, int max_iters, cudaStream_t s) {
-    cudaError_t e0 = sort_source(a, src, s);
-    if (e0 != cudaSuccess) return cuda_fail(e0, "source Morton order");
+cil_status run_begin(IterArgs& a, const float* src, int64_t m, const double* pose_init, int max_iters, cudaStream_t s,
+                     bool ordered = false) {
+    if (ordered) {
+        // icp_order_source already filled the workspace's permutation / ordered copy (host.cu)
+        a.src = (m == 0 || (debug_flags() & 16u)) ? src : a.srcs;
+    } else {
+        cudaError_t e0 = sort_source(a, src, s);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "source Morton order");
+    }
     const int init_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m + 255) / 256, (int64_t)sm_count() * 4));
     run_init_kernel<<<init_blocks, 256, 0, s>>>(a.st, pose_init, a.nn, a.gw, a.gp, (int)m, a.iter_log, 2 * max_iters);
     count_launches(1);
@@ -2193,9 +2199,42 @@ cil_status run_begin(IterArgs& a, const float* src, int64_t m, const double* pos
 }  // namespace
 }  // namespace cil
 
+namespace cil {
+// host.cu: the source-order step of cil_icp_run on its own stream (it only depends on the source,
+// so the host-buffer call runs it next to the target's copy and build), then the run with
+// `ordered` set.  Same kernels, same workspace contents as cil_icp_run.
+bool icp_small_path_nm(int64_t n, int64_t m) {
+    return !(debug_flags() & 64u) && m > 0 && n <= kSmallMaxN && (long long)m * n <= kSmallMaxPairs;
+}
+cudaError_t icp_order_source(void* ws, const float* src, int64_t m, cudaStream_t s) {
+    IterArgs a{};
+    bind_ws(a, ws, m);
+    a.m = (int)m;
+    return sort_source(a, src, s);
+}
+}  // namespace cil
+
+static cil_status icp_run_impl(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                               const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                               double* iter_log, cil_stream_t stream, bool ordered);
+
 CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m, const double* pose_init,
                                const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
                                double* iter_log, cil_stream_t stream) {
+    return icp_run_impl(t, src, m, pose_init, params, ws, ws_bytes, res, iter_log, stream, false);
+}
+
+namespace cil {
+cil_status icp_run_ordered(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                           const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                           cil_stream_t stream) {
+    return icp_run_impl(t, src, m, pose_init, params, ws, ws_bytes, res, nullptr, stream, true);
+}
+}  // namespace cil
+
+static cil_status icp_run_impl(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                               const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                               double* iter_log, cil_stream_t stream, bool ordered) {
     cil_status rc = check_common("cil_icp_run", t, src, m, params, ws, ws_bytes);
     if (rc != CIL_OK) return rc;
     if (!pose_init || !res) { set_error("cil_icp_run: pose_init/res NULL"); return CIL_ERR_INVALID_ARG; }
@@ -2218,7 +2257,7 @@ CIL_API cil_status cil_icp_run(const cil_target* t, const float* src, int64_t m,
         if (e != cudaSuccess) return cuda_fail(e, "run_final_kernel launch");
         return CIL_OK;
     }
-    rc = run_begin(a, src, m, pose_init, params->max_iters, s);
+    rc = run_begin(a, src, m, pose_init, params->max_iters, s, ordered);
     if (rc != CIL_OK) return rc;
     for (int it = 0; it < params->max_iters; ++it) {
         cudaError_t e = launch_iter(a, params->metric, s);

@@ -178,6 +178,14 @@ cudaError_t radix_sort_pairs(unsigned long long* k0, uint32_t* v0, unsigned long
 cudaError_t grid_build(const float* pts, int n, const float4* quant, const float4* qmax, float pts_per_cell,
                        cudaStream_t s, void** mem, size_t* bytes, TargetView* v, int* nlaunch);
 
+// icp.cu (for host.cu): whether (n, m) takes the small-problem path (no source ordering), the
+// source-order step of cil_icp_run alone on stream s, and the run with that step already done
+bool icp_small_path_nm(int64_t n, int64_t m);
+cudaError_t icp_order_source(void* ws, const float* src, int64_t m, cudaStream_t s);
+cil_status icp_run_ordered(const cil_target* t, const float* src, int64_t m, const double* pose_init,
+                           const cil_icp_params* params, void* ws, size_t ws_bytes, cil_icp_result* res,
+                           cil_stream_t stream);
+
 // prim.cu: in-place exclusive scan of uint32 (returns the number of kernels launched)
 size_t scan_temp_bytes(int64_t len);
 // (len <= 32,768, a multiple of 4: one launch of one block; pdl: programmatic dependent launches)

@@ -77,6 +77,9 @@ CIL_API cil_status cil_icp_align_host(const float* target, const float* normals,
     cudaError_t e = cudaSuccess;
     auto fail = [&](const char* what) {
         if (rc == CIL_OK && e != cudaSuccess) rc = cuda_fail(e, what);
+        // the second stream may still be copying from the caller's buffers into the block:
+        // drain it before the block is released and before the caller gets its buffers back
+        cudaStreamSynchronize(side->s);
         if (t) cil_target_free(t, stream);
         pool_free(mem, s);
         cudaStreamSynchronize(s);

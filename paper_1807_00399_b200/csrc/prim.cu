@@ -8,8 +8,11 @@ namespace cil {
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;                          // per thread
-constexpr int kScanTile = kScanThreads * kScanItems;    // 4096 per block
+#ifndef CIL_SCAN_ITEMS
+#define CIL_SCAN_ITEMS 4      // (tiles of 1,024 counters: C4 build 0.426 -> 0.410 ms; 16: 0.426, 8: 0.414, 2: 0.400 but 2^24 build +2.6 %)
+#endif
+constexpr int kScanItems = CIL_SCAN_ITEMS;                          // per thread
+constexpr int kScanTile = kScanThreads * kScanItems;    // 1024 per block
 #ifndef CIL_SCAN_FUSED_PREFIX
 #define CIL_SCAN_FUSED_PREFIX 1
 #endif
